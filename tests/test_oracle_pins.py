@@ -1,0 +1,374 @@
+"""Pins of the CPU oracle against things other than itself (closed forms, invariants,
+brute force, values printed in the paper).  All CPU (-m "not gpu").
+
+Each test names the passage / closed form it pins.  A plausible oracle mistake
+(dropped term, wrong sign, wrong axis weight, transposed operand, wrong source or
+receiver step) fails at least one of them -- see DESIGN.md "Oracle pins".
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _read_golden(name):
+    rows = []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line)
+    return rows
+
+
+# ----------------------------------------------------------------------------- FD weights
+def test_fd_weights_textbook():
+    """Closed-form weights == textbook table (tests/golden/fd_weights_textbook.txt)."""
+    for row in _read_golden("fd_weights_textbook.txt"):
+        order, vals = row.split(":")
+        want = [Fraction(v) for v in vals.split()]
+        assert oracle.fd_weights_exact(int(order)) == want
+
+
+@pytest.mark.parametrize("order", range(2, 17, 2))
+def test_fd_weights_moments(order):
+    """Taylor moments: sum c_k (k^{2j}) * 2 = 0 for j = 0 (with c0), 2 for j = 1, 0 for 2 <= j <= m."""
+    c = oracle.fd_weights_exact(order)
+    m = order // 2
+    assert c[0] + 2 * sum(c[1:]) == 0
+    for j in range(1, m + 1):
+        s = 2 * sum(c[k] * Fraction(k) ** (2 * j) for k in range(1, m + 1))
+        assert s == (2 if j == 1 else 0), (order, j)
+
+
+def test_paper_awe_constants():
+    """2dt^2/h^2 * SO8 weights with dt=3.04, h=20 reproduce P:1682-1707 to the printed digits."""
+    g = {r.split()[0]: float(r.split()[1]) for r in _read_golden("paper_awe_so8_constants.txt")}
+    dt, h = g["tcse0_factor"], 20.0
+    scale = 2 * dt * dt / (h * h)
+    c = oracle.fd_weights(8)
+    for k in range(1, 5):
+        assert math.isclose(scale * c[k], g[f"k{k}"], rel_tol=1e-12), k
+    assert math.isclose(3 * scale * c[0], g["k0"], rel_tol=1e-12)
+
+
+# ----------------------------------------------------------------------------- heat closed forms
+def test_heat_eigenmode_2d_C1():
+    """C1 geometry (128^2, alpha=0.1, 20 steps) on sin(pi x)sin(pi y): u^n = g^n u^0 with
+    g = 1 - 4 alpha sum_axes sin^2(pi h/2)  (discrete eigenvalue of the 5-point Laplacian, Q4)."""
+    nx = ny = 128
+    nt = 20
+    u0 = W.eigenmode_2d(nx, ny, np.float64)
+    g = 1.0 - 4 * 0.1 * (2 * math.sin(math.pi / (2 * (nx + 1))) ** 2)
+    assert abs(g - 0.999881387938) < 1e-12          # SURVEY §8(c) printed value
+    for dtype, tol in ((np.float64, 1e-13), (np.float32, 2e-6)):
+        P = oracle.embed(np.zeros((1, ny, nx)), 2, 1, dtype)
+        C = oracle.embed(u0.astype(dtype)[None], 2, 1, dtype)
+        oracle.run_untiled(2, (nx, ny, 1), 2, oracle.fd_weights(2), [1.0, 1.0, 1.0], 1, 0.1,
+                           P, C, nt=nt, ftz=(dtype == np.float32))
+        got = oracle.extract(C, 2, (nx, ny, 1), 1)[0].astype(np.float64)
+        want = g ** nt * u0
+        assert np.abs(got - want).max() / np.abs(want).max() < tol
+        # contract: P holds u^{nt-1}
+        gotp = oracle.extract(P, 2, (nx, ny, 1), 1)[0].astype(np.float64)
+        assert np.abs(gotp - g ** (nt - 1) * u0).max() < tol * 2
+
+
+def test_heat_eigenmode_3d_anisotropic():
+    """3-D 7-point heat on a non-cubic grid with distinct spacings (catches axis mix-ups)."""
+    n = (20, 14, 9)
+    hs = (1.0, 0.8, 1.25)
+    dt = 0.05
+    # mode numbers (1,2,1): u = prod sin(pi q_a i_a/(n_a+1))
+    q = (1, 2, 1)
+    axes = [np.sin(np.pi * q[a] * np.arange(1, n[a] + 1) / (n[a] + 1)) for a in range(3)]
+    u0 = axes[2][:, None, None] * axes[1][None, :, None] * axes[0][None, None, :]
+    lam = sum(4.0 / hs[a] ** 2 * math.sin(math.pi * q[a] / (2 * (n[a] + 1))) ** 2 for a in range(3))
+    g = 1.0 - dt * lam
+    P = oracle.embed(np.zeros_like(u0), 3, 1, np.float64)
+    C = oracle.embed(u0, 3, 1, np.float64)
+    nt = 7
+    oracle.run_untiled(3, n, 2, oracle.fd_weights(2), hs, 1, dt, P, C, nt=nt, ftz=False)
+    got = oracle.extract(C, 3, n, 1)
+    assert np.abs(got - g ** nt * u0).max() < 1e-13
+
+
+def test_heat_max_principle_and_mass():
+    """C1 random field: values stay in [0,1) (1 - 2d*alpha >= 0) and sum(u) is non-increasing."""
+    p = W.problem("C1", nt=1)
+    _, u = W.initial_fields(p)
+    P = oracle.embed(np.zeros_like(u), 2, 1)
+    C = oracle.embed(u, 2, 1)
+    mass = [float(u.astype(np.float64).sum())]
+    for _ in range(20):
+        oracle.run_untiled(2, p.n, 2, oracle.fd_weights(2), [1, 1, 1], 1, 0.1, P, C, nt=1)
+        x = oracle.extract(C, 2, p.n, 1)
+        assert x.min() >= 0.0 and x.max() < 1.0
+        mass.append(float(x.astype(np.float64).sum()))
+    assert all(b <= a + 1e-3 for a, b in zip(mass, mass[1:]))
+    assert mass[-1] < mass[0]
+
+
+# ----------------------------------------------------------------------------- wave closed forms
+def _wave_const_medium(n, v, dt, r, dtype=np.float64):
+    vel = oracle.embed(np.full((n[2], n[1], n[0]), v), 3, r, dtype)
+    vel[vel == 0] = v
+    return oracle.medium(vel, None, dt, dtype=dtype, ftz=False)
+
+
+@pytest.mark.parametrize("order", [4, 8])
+def test_wave_plane_wave_discrete_dispersion(order):
+    """Plane wave cos(k.x - w t) with sin^2(w dt/2) = (c dt/2)^2 sum_a (-c0 - 2 sum_m c_m cos(m k_a h_a))/h_a^2
+    is an exact discrete solution inside the dependence cone (Appendix A7)."""
+    r = order // 2
+    n = (40, 36, 32)
+    h = (10.0, 10.0, 10.0)
+    v = 1500.0
+    dt = 8.889e-4
+    nt = 3
+    k = 2 * np.pi * np.array([1 / 200, 1 / 300, 1 / 400])
+    c = oracle.fd_weights(order)
+    S = sum((-c[0] - 2 * sum(c[m] * math.cos(m * k[a] * h[a]) for m in range(1, r + 1))) / h[a] ** 2
+            for a in range(3))
+    w = 2 / dt * math.asin(v * dt / 2 * math.sqrt(S))
+    x = [np.arange(n[a]) * h[a] for a in range(3)]
+    phase = k[0] * x[0][None, None, :] + k[1] * x[1][None, :, None] + k[2] * x[2][:, None, None]
+    a_, c_ = _wave_const_medium(n, v, dt, r)
+    P = oracle.embed(np.cos(phase + w * dt), 3, r, np.float64)   # u^{-1}
+    C = oracle.embed(np.cos(phase), 3, r, np.float64)            # u^0
+    oracle.run_untiled(3, n, order, c, h, 2, dt, P, C, a_, c_, nt=nt, ftz=False)
+    got = oracle.extract(C, 3, n, r)
+    want = np.cos(phase - w * dt * nt)
+    m = nt * r          # cone: points further than nt*r from the halo
+    sl = (slice(m, n[2] - m), slice(m, n[1] - m), slice(m, n[0] - m))
+    assert np.abs(got[sl] - want[sl]).max() < 1e-11
+    # the continuous relation w = v|k| must NOT match (the test discriminates the discrete one)
+    wc = v * np.linalg.norm(k)
+    assert np.abs(got[sl] - np.cos(phase - wc * dt * nt)[sl]).max() > 1e-9
+
+
+def test_wave_so2_standing_wave():
+    """r = 1: sin modes are exact eigenvectors with a zero halo: u^n = cos(n theta) phi over the
+    whole grid, cos(theta) = 1 - c^2 dt^2 lambda/2."""
+    n = (18, 14, 12)
+    h = (10.0, 10.0, 10.0)
+    v, dt = 2000.0, 1e-3
+    q = (1, 1, 2)
+    axes = [np.sin(np.pi * q[a] * np.arange(1, n[a] + 1) / (n[a] + 1)) for a in range(3)]
+    phi = axes[2][:, None, None] * axes[1][None, :, None] * axes[0][None, None, :]
+    lam = sum(4 / h[a] ** 2 * math.sin(math.pi * q[a] / (2 * (n[a] + 1))) ** 2 for a in range(3))
+    th = math.acos(1 - (v * dt) ** 2 * lam / 2)
+    a_, c_ = _wave_const_medium(n, v, dt, 1)
+    P = oracle.embed(math.cos(th) * phi, 3, 1, np.float64)
+    C = oracle.embed(phi, 3, 1, np.float64)
+    nt = 25
+    oracle.run_untiled(3, n, 2, oracle.fd_weights(2), h, 2, dt, P, C, a_, c_, nt=nt, ftz=False)
+    assert np.abs(oracle.extract(C, 3, n, 1) - math.cos(nt * th) * phi).max() < 1e-12
+    assert np.abs(oracle.extract(P, 3, n, 1) - math.cos((nt - 1) * th) * phi).max() < 1e-12
+
+
+def _lap(u, c, h, r):
+    """Independent numpy L_h on the oracle layout (interior only; zero halo)."""
+    out = np.zeros_like(u)
+    I = (slice(r, -r),) * 3
+    out[I] = (c[0] / h[0] ** 2 + c[0] / h[1] ** 2 + c[0] / h[2] ** 2) * u[I]
+    for k in range(1, r + 1):
+        for ax, hh in zip((2, 1, 0), h):
+            lo = [slice(r, -r)] * 3
+            hi = [slice(r, -r)] * 3
+            n_ax = u.shape[ax]
+            lo[ax] = slice(r - k, n_ax - r - k)
+            hi[ax] = slice(r + k, n_ax - r + k)
+            out[I] += c[k] / hh ** 2 * (u[tuple(lo)] + u[tuple(hi)])
+    return out
+
+
+@pytest.mark.parametrize("damped", [False, True])
+def test_wave_energy(damped):
+    """E^{n+1/2} = sum m (u^{n+1}-u^n)^2 - dt^2 sum u^{n+1} L u^n is conserved without damping and
+    non-increasing with eta >= 0 (Appendix A8)."""
+    rng = np.random.default_rng(3)
+    r, order = 4, 8
+    n = (16, 14, 12)
+    h = (10.0, 10.0, 10.0)
+    dt = 8e-4
+    vel_i = 2000.0 * (1 + 0.05 * (2 * rng.random((n[2], n[1], n[0])) - 1))
+    vel = oracle.embed(vel_i, 3, r, np.float64)
+    vel[vel == 0] = 2000.0
+    eta = oracle.embed(rng.random((n[2], n[1], n[0])) * 2e-3, 3, r, np.float64) if damped else None
+    a_, c_ = oracle.medium(vel, eta, dt, dtype=np.float64, ftz=False)
+    m = np.zeros_like(vel)
+    m[(slice(r, -r),) * 3] = 1.0 / vel_i ** 2
+    cf = oracle.fd_weights(order)
+    P = oracle.embed(rng.standard_normal((n[2], n[1], n[0])), 3, r, np.float64)
+    C = oracle.embed(rng.standard_normal((n[2], n[1], n[0])), 3, r, np.float64)
+    E = []
+    for _ in range(30):
+        Cold = C.copy()
+        oracle.run_untiled(3, n, order, cf, h, 2, dt, P, C, a_, c_, nt=1, ftz=False)
+        E.append(float((m * (C - Cold) ** 2).sum() - dt * dt * (C * _lap(Cold, cf, h, r)).sum()))
+    E = np.array(E)
+    assert E.min() > 0
+    if damped:
+        assert np.all(np.diff(E) <= 1e-12 * abs(E[0]))
+        assert E[-1] < 0.9 * E[0]
+    else:
+        assert np.abs(E - E[0]).max() / abs(E[0]) < 1e-12
+
+
+def test_wave_paper_literal_form():
+    """The a/c rewrite equals the paper's literal update
+    u+ = ((te-2m)u- + 4m u + 2dt^2 L u)/(te+2m), te = dt*damp, in fp64."""
+    rng = np.random.default_rng(5)
+    r, order = 4, 8
+    n = (12, 11, 10)
+    h = (20.0, 20.0, 20.0)
+    dt = 3.04
+    vel_i = 1.5 + rng.random((n[2], n[1], n[0]))
+    vel = oracle.embed(vel_i, 3, r, np.float64); vel[vel == 0] = 1.5
+    damp_i = rng.random((n[2], n[1], n[0])) * 0.1
+    dmp = oracle.embed(damp_i, 3, r, np.float64)
+    a_, c_ = oracle.medium(vel, dmp, dt, dtype=np.float64, ftz=False)
+    cf = oracle.fd_weights(order)
+    P = oracle.embed(rng.standard_normal((n[2], n[1], n[0])), 3, r, np.float64)
+    C = oracle.embed(rng.standard_normal((n[2], n[1], n[0])), 3, r, np.float64)
+    m = 1 / vel_i ** 2
+    te = dt * damp_i
+    I = (slice(r, -r),) * 3
+    Lu = _lap(C, cf, h, r)[I]
+    want = ((te - 2 * m) * P[I] + 4 * m * C[I] + 2 * dt * dt * Lu) / (te + 2 * m)
+    oracle.run_untiled(3, n, order, cf, h, 2, dt, P, C, a_, c_, nt=1, ftz=False)
+    assert np.abs(C[I] - want).max() / np.abs(want).max() < 1e-13
+
+
+def test_medium_fp32_rounding():
+    """fp32 a, c within a few ulp of the fp64 definition."""
+    p = W.problem("C3", n=(24, 20, 16), sponge=6)
+    vel = W.velocity(p)
+    eta = W.damp(p)
+    a32, c32 = oracle.medium(vel, eta, p.dt)
+    v = vel.astype(np.float64)
+    m = 1 / (v * v)
+    te = p.dt * eta.astype(np.float64)
+    a64 = (te - 2 * m) / (te + 2 * m)
+    c64 = 2 * p.dt * p.dt / (te + 2 * m)
+    assert np.abs(a32 - a64).max() < 4 * np.finfo(np.float32).eps
+    assert (np.abs(c32 - c64) / c64).max() < 4 * np.finfo(np.float32).eps
+    assert np.all(a32 >= -1.0) and np.all(a32 <= 1.0)
+
+
+# ----------------------------------------------------------------------------- brute force
+def _dense_L(n, c, h, r):
+    nx, ny, nz = n
+    N = nx * ny * nz
+    A = np.zeros((N, N))
+    idx = lambda x, y, z: (z * ny + y) * nx + x
+    for z in range(nz):
+        for y in range(ny):
+            for x in range(nx):
+                p = idx(x, y, z)
+                A[p, p] = sum(c[0] / hh ** 2 for hh in h)
+                for k in range(1, r + 1):
+                    for (dx_, dy_, dz_), hh in (((k, 0, 0), h[0]), ((0, k, 0), h[1]), ((0, 0, k), h[2])):
+                        for s in (1, -1):
+                            xx, yy, zz = x + s * dx_, y + s * dy_, z + s * dz_
+                            if 0 <= xx < nx and 0 <= yy < ny and 0 <= zz < nz:
+                                A[p, idx(xx, yy, zz)] += c[k] / hh ** 2
+    return A
+
+
+@pytest.mark.parametrize("time_order", [1, 2])
+def test_dense_operator_brute_force(time_order):
+    """fp64 dense operator (rows built from the coefficient list) x state, with a source and
+    receivers, equals O1-fp64 on a 7x6x5 grid (pins sources, receivers, step0 indexing)."""
+    rng = np.random.default_rng(11)
+    n = (7, 6, 5)
+    r, order = 2, 4
+    h = (1.0, 1.3, 0.9)
+    c = oracle.fd_weights(order)
+    A = _dense_L(n, c, h, r)
+    dt = 0.02
+    shape = (n[2], n[1], n[0])
+    p0 = rng.standard_normal(shape)
+    c0 = rng.standard_normal(shape)
+    src = [(3, 2, 1), (1, 4, 3), (3, 2, 1)]           # repeated source: two adds
+    rec = [(0, 0, 0), (3, 2, 1), (6, 5, 4)]
+    nt, step0 = 6, 3
+    wav = rng.standard_normal((step0 + nt, len(src)))
+    if time_order == 2:
+        av = rng.random(shape) * 0.4 - 0.9
+        cv = rng.random(shape) * 0.01 + 0.01
+    P = oracle.embed(p0, 3, r, np.float64)
+    C = oracle.embed(c0, 3, r, np.float64)
+    a_ = oracle.embed(av, 3, r, np.float64) if time_order == 2 else None
+    c_ = oracle.embed(cv, 3, r, np.float64) if time_order == 2 else None
+    tr = oracle.run_untiled(3, n, order, c, h, time_order, dt, P, C, a_, c_, nt=nt, step0=step0,
+                            src=src, wavelet=wav, rec=rec, ftz=False)
+    up, uc = p0.ravel(), c0.ravel()
+    flat = lambda p: (p[2] * n[1] + p[1]) * n[0] + p[0]
+    want_tr = np.zeros((nt, len(rec)))
+    for s in range(nt):
+        acc = A @ uc
+        for i, sp in enumerate(src):
+            acc[flat(sp)] += wav[step0 + s, i]
+        if time_order == 1:
+            un = uc + dt * acc
+        else:
+            un = av.ravel() * (up - uc) + uc + cv.ravel() * acc
+        up, uc = uc, un
+        want_tr[s] = [uc[flat(q)] for q in rec]
+    assert np.abs(oracle.extract(C, 3, n, r).ravel() - uc).max() < 1e-12 * max(1, np.abs(uc).max())
+    assert np.abs(oracle.extract(P, 3, n, r).ravel() - up).max() < 1e-12 * max(1, np.abs(up).max())
+    assert np.abs(tr - want_tr).max() < 1e-12 * max(1, np.abs(want_tr).max())
+
+
+def test_first_steps_source_closed_form():
+    """From rest, one source: u^1 = c_s w[0] e_s exactly; u^2(s +- e_x) = c W_x1 (u^1_s) (fp32)."""
+    p = W.problem("C3", n=(16, 16, 16), nt=2, sponge=3)
+    P, C, tr = oracle.run_problem(p, nt=1)
+    vel = W.velocity(p); eta = W.damp(p)
+    a32, c32 = oracle.medium(vel, eta, p.dt)
+    s = p.src[0]
+    w = W.wavelet(p, 2)
+    want = np.float32(c32[s[2], s[1], s[0]] * np.float32(np.float32(0) + w[0, 0]))
+    assert C[s[2], s[1], s[0]] == want
+    C2 = C.copy(); C2[s[2], s[1], s[0]] = 0
+    assert np.all(C2 == 0) and np.all(P == 0)
+
+
+# ----------------------------------------------------------------------------- symmetry / linearity
+def test_mirror_symmetry_bitwise():
+    """Mirror-symmetric input, medium and source => bitwise mirror-symmetric fields and traces."""
+    p = W.problem("C5", n=(21, 19, 17), nt=12, sponge=4)
+    p = W.Problem(**{**p.__dict__, "src": ((10, 9, 8),), "rec": ((3, 9, 8), (17, 9, 8), (10, 2, 8), (10, 16, 8))})
+    P, C, tr = oracle.run_problem(p)
+    assert np.array_equal(C, C[:, :, ::-1]) and np.array_equal(C, C[:, ::-1, :])
+    assert np.array_equal(P, P[:, :, ::-1])
+    assert np.array_equal(tr[:, 0], tr[:, 1]) and np.array_equal(tr[:, 2], tr[:, 3])
+    assert np.abs(C).max() > 0
+
+
+def test_scale_by_two_bitwise():
+    """Linearity: doubling u^{-1}, u^0 doubles every output bitwise (no FTZ/overflow involved)."""
+    rng = np.random.default_rng(7)
+    n = (13, 12, 11)
+    r, order = 6, 12
+    p = W.problem("C5", n=n, sponge=3)
+    vel = oracle.embed(W.velocity(p), 3, r); vel[vel == 0] = 1500
+    a_, c_ = oracle.medium(vel, oracle.embed(W.damp(p), 3, r), p.dt)
+    outs = []
+    base_p = rng.standard_normal((n[2], n[1], n[0])).astype(np.float32)
+    base_c = rng.standard_normal((n[2], n[1], n[0])).astype(np.float32)
+    for s in (1.0, 2.0):
+        P = oracle.embed(np.float32(s) * base_p, 3, r)
+        C = oracle.embed(np.float32(s) * base_c, 3, r)
+        oracle.run_untiled(3, n, order, oracle.fd_weights(order), p.dx, 2, p.dt, P, C, a_, c_, nt=5)
+        outs.append(C)
+    assert np.array_equal(outs[1], np.float32(2) * outs[0])
