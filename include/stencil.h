@@ -1,0 +1,132 @@
+/*
+ * stencil.h -- C ABI of libstencil.so, the B200 (sm_100a) time-tiled FD stencil sweep.
+ *
+ * What the library computes (PAPER.md = arXiv 1707.02347; "P:n" = line n of PAPER.md;
+ * SURVEY.md §8 is the scope table):
+ *
+ *   The time-stepped explicit finite-difference star-stencil sweep Devito generates
+ *   (P:519-556 diffusion, P:1671-1719 damped acoustic wave), restructured by time
+ *   tiling: several time levels are computed per pass of a
+ *   z-streamed on-chip window, with the streamed axis skewed by the stencil radius per
+ *   level ("skew each loop ... by the negated value of the greatest
+ *   negative dependence") and x-y tiles overlapped by the radius per level.
+ *
+ *   Per interior point p and step n (canonical order, normative):
+ *       acc = K0 * u^n[p]
+ *       for k = 1..r:  for axis in (x, y, z):
+ *           acc = fma(W_axis_k, u^n[p - k e_axis] + u^n[p + k e_axis], acc)
+ *       for each source s located at p, in index order:  acc = acc + wavelet[step0+n][s]
+ *       heat (time_order 1):  u^{n+1}[p] = fma(dt, acc, u^n[p])
+ *       wave (time_order 2):  u^{n+1}[p] = fma(c[p], acc, fma(a[p], u^{n-1}[p] - u^n[p], u^n[p]))
+ *   with W_axis_k = (float)(coeffs[k] / dx[axis]^2), K0 = (float)(sum_axes coeffs[0]/dx[axis]^2)
+ *   (double arithmetic, axes summed x, y, z), and per-point medium
+ *       m = 1/(v*v),  te = (float)dt * damp,  a = (te - 2m)/(te + 2m),  c = (float)(2 dt^2)/(te + 2m)
+ *   which is the paper's  u^{n+1} = ((te-2m) u^{n-1} + 4m u^n + 2dt^2 L u^n)/(te+2m)  rewritten
+ *   exactly (4m/(te+2m) = 1-a).  All fp32 with denormals flushed (P:570-576 DLE flush).
+ *   Points outside the global interior are zero (Dirichlet, never stored or read).
+ *
+ * Layout (stencil_layout): every field is fp32 [Z][Y][X], x fastest, caller-allocated:
+ *     X = round_up(nx, 32)        (128-byte rows; columns >= nx are padding, never read as data)
+ *     Y = ny                      (no y halo: the boundary is implicit)
+ *     Z = nz_local + 2*G          (G = radius*t_comm ghost planes on each side when nranks > 1,
+ *                                  G = 0 when nranks == 1; 2-D problems: Z = 1)
+ *   interior point (x, y, z_local) lives at [G + z_local][y][x].
+ *
+ * Ownership: the caller owns every field, wavelet and trace.  The library owns the plan and
+ * its device scratch (medium a/c in an interleaved layout, the ping-pong pair for
+ * t_kernel > 1, source/receiver tables).  It never frees caller memory.
+ *
+ * Errors: every entry returns st_status; nothing aborts, exits or throws across the ABI.
+ * The message of the last failure is available from stencil_last_error().
+ * A plan is not thread-safe: use one plan per (thread, device, stream).
+ */
+#ifndef PAPER_1707_02347_B200_STENCIL_H
+#define PAPER_1707_02347_B200_STENCIL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct stencil_plan stencil_plan;   /* opaque, owned by the library */
+
+typedef enum {
+  ST_OK = 0,
+  ST_EINVAL = 1,          /* bad argument (null pointer, radius, sizes, coordinates, nt) */
+  ST_ENOMEM = 2,          /* device or host allocation failed */
+  ST_ECUDA = 3,           /* a CUDA runtime/driver call failed (message has the CUDA error) */
+  ST_EUNSUPPORTED = 5,    /* (radius, t_kernel, ndim, time_order) not compiled into this build */
+  ST_ESTATE = 6           /* plan is in an error state after an asynchronous failure */
+} st_status;
+
+enum { ST_FTZ = 1u };     /* flush denormals (required; the only arithmetic mode built) */
+
+typedef struct {
+  int32_t ndim;           /* 2 or 3 */
+  int64_t n[3];           /* GLOBAL interior points (nx, ny, nz); nz = 1 when ndim == 2 */
+  int32_t radius;         /* 1..8  (space order 2..16) */
+  const double *coeffs;   /* host, radius+1 unscaled 2nd-derivative weights c0..cr (copied) */
+  int32_t time_order;     /* 1: heat u' = u + dt*L u ; 2: damped leapfrog wave */
+  double dt;
+  double dx[3];           /* grid spacing per axis (dx[2] ignored for 2-D) */
+  int32_t t_kernel;       /* on-chip time-tile depth T_k (1 = untiled) */
+  int32_t t_comm;         /* halo depth in steps T_c (>= 1), multiple of T_k; used when nranks > 1 */
+  int32_t rank, nranks;   /* z-slab index/count; n[2] % nranks == 0 */
+  int32_t device;         /* CUDA device ordinal */
+  void *stream;           /* cudaStream_t all work is enqueued on (NULL = legacy default) */
+  uint32_t flags;         /* ST_FTZ (must be set) */
+} st_config;
+
+/* Validate cfg, pick the compiled kernel instance, allocate scratch.  *out = NULL on error.
+ * Errors: ST_EINVAL (null cfg/out/coeffs, ndim, radius outside 1..8, t_kernel < 1,
+ * t_comm % t_kernel != 0 when nranks > 1, n[2] % nranks != 0, rank outside [0,nranks)),
+ * ST_EUNSUPPORTED (instance not built, ST_FTZ cleared), ST_ECUDA, ST_ENOMEM. */
+st_status stencil_create(const st_config *cfg, stencil_plan **out);
+
+/* padded = {X, Y, Z}; interior_origin = {0, 0, G}; z_global_range = global interior planes
+ * [z0, z1) owned by this rank.  Any output pointer may be NULL. */
+st_status stencil_layout(const stencil_plan *p, int64_t padded[3], int64_t interior_origin[3],
+                         int64_t z_global_range[2]);
+
+/* Advance (u_prev, u_cur) = (u^{n-1}, u^n) -> (u^{n+nt-1}, u^{n+nt}) in place.
+ *   u_prev, u_cur : device, layout above, read/write.  heat: u_prev input ignored.
+ *   vel, damp     : device, layout above; wave only (damp may be NULL = 0).  Must be valid on
+ *                   every interior and ghost plane read (z-slabs: ghost planes included).
+ *   nt >= 0 steps; step0 = global index of the first step (indexes the wavelet rows).
+ *   src_xyz       : host int32 [nsrc][3], GLOBAL interior coordinates (x, y, z)
+ *   src_wavelet   : device fp32 [step0 + nt rows at least][nsrc]
+ *   rec_xyz       : host int32 [nrec][3], GLOBAL interior coordinates
+ *   rec_trace     : device fp32 [nt][nrec]; row n = u^{n+1} at each receiver this rank owns;
+ *                   entries of receivers owned by other ranks are not written.
+ * nranks > 1: the caller must have exchanged ghost planes before the call (depth
+ *   radius*nt of u_cur and radius*(nt-1) of u_prev), and nt <= t_comm.
+ * Asynchronous on cfg.stream; arguments must stay valid until it completes.
+ * Errors: ST_EINVAL (null required pointer, nt < 0, nt > t_comm with nranks > 1, a source or
+ * receiver outside the global interior), ST_ESTATE, ST_ECUDA, ST_ENOMEM. */
+st_status stencil_run(stencil_plan *p, float *u_prev, float *u_cur, const float *vel,
+                      const float *damp, int32_t nt, int64_t step0, int32_t nsrc,
+                      const int32_t *src_xyz, const float *src_wavelet, int32_t nrec,
+                      const int32_t *rec_xyz, float *rec_trace);
+
+/* Wait for the plan's stream; surfaces asynchronous CUDA errors (then ST_ECUDA, and the plan
+ * enters ST_ESTATE). */
+st_status stencil_sync(stencil_plan *p);
+
+/* Frees scratch; NULL-safe; never touches caller memory. */
+void stencil_destroy(stencil_plan *p);
+
+/* Last error message of p, or (p == NULL) the thread-local message of the last failed
+ * stencil_create / argument check.  Never NULL. */
+const char *stencil_last_error(const stencil_plan *p);
+
+/* Pure host query (no device needed): is (ndim, time_order, radius, t_kernel) compiled? */
+int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel);
+
+/* Pure host query: library ABI version (major*100 + minor). */
+int32_t stencil_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAPER_1707_02347_B200_STENCIL_H */

@@ -1,0 +1,87 @@
+"""ctypes binding of libstencil.so (include/stencil.h).  Argument marshalling only.
+
+The library is the product: there is no CPU fallback.  If libstencil.so is missing or cannot
+be loaded, every entry point raises -- loudly -- instead of computing anything elsewhere.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libstencil.so")
+
+ST_OK, ST_EINVAL, ST_ENOMEM, ST_ECUDA, ST_EUNSUPPORTED, ST_ESTATE = 0, 1, 2, 3, 5, 6
+ST_FTZ = 1
+STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 5: "ST_EUNSUPPORTED",
+                6: "ST_ESTATE"}
+
+# Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
+EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_sync", "stencil_destroy",
+           "stencil_last_error", "stencil_supported", "stencil_abi_version")
+
+
+class StConfig(ctypes.Structure):
+    _fields_ = [
+        ("ndim", ctypes.c_int32),
+        ("n", ctypes.c_int64 * 3),
+        ("radius", ctypes.c_int32),
+        ("coeffs", ctypes.POINTER(ctypes.c_double)),
+        ("time_order", ctypes.c_int32),
+        ("dt", ctypes.c_double),
+        ("dx", ctypes.c_double * 3),
+        ("t_kernel", ctypes.c_int32),
+        ("t_comm", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("nranks", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+class StencilError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load():
+    """Load libstencil.so (raises if it is absent: build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not found: the CUDA extension is not built "
+                           "(run `python -c 'import __graft_entry__ as g; g.build()'`); "
+                           "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    lib.stencil_create.argtypes = [ctypes.POINTER(StConfig), ctypes.POINTER(P)]
+    lib.stencil_create.restype = ctypes.c_int
+    lib.stencil_layout.argtypes = [P, ctypes.c_int64 * 3, ctypes.c_int64 * 3, ctypes.c_int64 * 2]
+    lib.stencil_layout.restype = ctypes.c_int
+    lib.stencil_run.argtypes = [P, P, P, P, P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, P, P,
+                                ctypes.c_int32, P, P]
+    lib.stencil_run.restype = ctypes.c_int
+    lib.stencil_sync.argtypes = [P]
+    lib.stencil_sync.restype = ctypes.c_int
+    lib.stencil_destroy.argtypes = [P]
+    lib.stencil_destroy.restype = None
+    lib.stencil_last_error.argtypes = [P]
+    lib.stencil_last_error.restype = ctypes.c_char_p
+    lib.stencil_supported.argtypes = [ctypes.c_int32] * 4
+    lib.stencil_supported.restype = ctypes.c_int32
+    lib.stencil_abi_version.argtypes = []
+    lib.stencil_abi_version.restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+def check(status: int, plan=None):
+    if status != ST_OK:
+        msg = load().stencil_last_error(plan)
+        raise StencilError(status, (msg or b"").decode(errors="replace"))

@@ -1,0 +1,141 @@
+"""Build libstencil.so (sm_100a) in-tree: generated kernel-instance TUs + abi.cu, nvcc in parallel.
+
+python -m paper_1707_02347_b200.build [--force] [-j N]
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import hashlib
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libstencil.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-Xptxas", "-v", "-I", os.path.join(HERE, "..", "include")]
+
+
+def _vy_nwy(ndim: int, R: int, TK: int):
+    """Register blocking per instance: queues hold TK*(2R+1)*VY packed pairs per thread."""
+    if ndim == 2:
+        return 4, 8
+    if TK * (2 * R + 1) * 4 <= 72:
+        return 4, 8
+    return 2, 12
+
+
+def instances():
+    """(ndim, wave, R, TK, VY, NWY) compiled into this build."""
+    out = []
+    for wave in (0, 1):
+        for R in range(1, 9):
+            for TK in (1, 2):
+                out.append((3, wave, R, TK) + _vy_nwy(3, R, TK))
+        for R in range(1, 9):
+            out.append((2, wave, R, 1) + _vy_nwy(2, R, 1))
+        out.append((2, wave, 1, 2) + _vy_nwy(2, 1, 2))
+        out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4))
+    for R, TK in ((1, 4), (2, 4), (1, 8)):
+        out.append((3, 0, R, TK) + _vy_nwy(3, R, TK))
+    return out
+
+
+def _gen_sources(groups: int):
+    os.makedirs(BUILD, exist_ok=True)
+    inst = instances()
+    files = []
+    per = [inst[i::groups] for i in range(groups)]
+    for gi, group in enumerate(per):
+        lines = ['#include "registry.h"', "namespace st {", f"extern const KernelEntry kInst{gi}[] = {{"]
+        for (ndim, wave, R, TK, VY, NWY) in group:
+            lines.append(f"  make_entry<{R}, {TK}, {'true' if wave else 'false'}, {ndim}, {VY}, {NWY}>(),")
+        lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]
+        files.append((os.path.join(BUILD, f"inst_{gi}.cu"), "\n".join(lines)))
+    reg = ['#include "registry.h"', "#include <vector>", "namespace st {"]
+    for gi in range(groups):
+        reg.append(f"extern const KernelEntry kInst{gi}[]; extern const int kInst{gi}Count;")
+    reg.append("static std::vector<KernelEntry> build_all() {\n  std::vector<KernelEntry> v;")
+    for gi in range(groups):
+        reg.append(f"  v.insert(v.end(), kInst{gi}, kInst{gi} + kInst{gi}Count);")
+    reg.append("  return v;\n}")
+    reg.append("static const std::vector<KernelEntry>& all() { static const std::vector<KernelEntry> v = build_all(); return v; }")
+    reg.append("const KernelEntry* registry_begin() { return all().data(); }")
+    reg.append("const KernelEntry* registry_end() { return all().data() + all().size(); }")
+    reg.append("const KernelEntry* find_kernel(int ndim, int time_order, int radius, int tk) {\n"
+               "  for (const auto& e : all())\n"
+               "    if (e.ndim == ndim && e.time_order == time_order && e.radius == radius && e.tk == tk) return &e;\n"
+               "  return nullptr;\n}")
+    reg += ["}  // namespace st", ""]
+    files.append((os.path.join(BUILD, "registry.cu"), "\n".join(reg)))
+    for path, text in files:
+        if not os.path.exists(path) or open(path).read() != text:
+            with open(path, "w") as f:
+                f.write(text)
+    return [f for f, _ in files]
+
+
+def _digest(paths):
+    h = hashlib.sha256()
+    for pth in sorted(paths):
+        with open(pth, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def _compile(src: str, log: bool):
+    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "registry.h"),
+            os.path.join(HERE, "..", "include", "stencil.h")]
+    stamp = obj + ".stamp"
+    d = _digest(deps)
+    if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == d:
+        return obj, ""
+    cmd = [NVCC] + ARCH + FLAGS + ["-I", CSRC, "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-6000:]}")
+    with open(stamp, "w") as f:
+        f.write(d)
+    return obj, r.stderr
+
+
+def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
+    groups = 12
+    srcs = _gen_sources(groups) + [os.path.join(CSRC, "abi.cu")]
+    if force:
+        for s in srcs:
+            o = os.path.join(BUILD, os.path.basename(s) + ".o")
+            if os.path.exists(o):
+                os.remove(o)
+    jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
+    objs, logs = [], []
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        for obj, log in ex.map(lambda s: _compile(s, verbose), srcs):
+            objs.append(obj)
+            logs.append(log)
+    if verbose:
+        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+            f.write("\n".join(logs))
+    need = force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)
+    if need:
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-j", type=int, default=0)
+    ap.add_argument("-v", action="store_true")
+    a = ap.parse_args()
+    print(build(force=a.force, jobs=a.j, verbose=a.v))

@@ -1,0 +1,538 @@
+// abi.cu -- plan, pass scheduling and the C ABI of libstencil.so (include/stencil.h).
+//
+// Host-side responsibilities:
+//   * layout (a1): fp32 [Z][Y][X], X = round_up(nx,32), no x/y halo storage (TMA OOB zero fill
+//     and in-kernel masks give the Dirichlet boundary), G = r*T_c ghost planes per z side for
+//     z-slabs;
+//   * medium precompute (a3): a, c per point once per run (kernel `medium_kernel`);
+//   * pass schedule (a7, a8): nt steps = passes of T_k levels (time-tiled kernel, ping-pong
+//     output pair) + single-level passes (in place), final swap/copy to honour the contract;
+//   * z-slab bookkeeping (a9): shrinking valid plane ranges between halo exchanges;
+//   * sources/receivers (a4, a5): filtered per slab, sorted by plane into per-plane tables.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/stencil.h"
+#include "registry.h"
+
+namespace {
+
+thread_local std::string g_err = "";
+
+struct Buf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct stencil_plan {
+  st_config cfg{};
+  std::vector<double> coeffs;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int sm_count = 148;
+  // layout
+  long long nx = 0, ny = 0, nzl = 0, X = 0, Y = 0, Z = 0, G = 0, z0g = 0;
+  bool has_lo = false, has_hi = false;
+  // kernels
+  const st::KernelEntry* k_tk = nullptr;   // time-tiled (t_kernel) instance
+  const st::KernelEntry* k_t1 = nullptr;   // single-level instance
+  int nslot_tk = 0, nslot_t1 = 0;
+  size_t smem_tk = 0, smem_t1 = 0;
+  int bps_tk = 1, bps_t1 = 1;
+  // coefficients
+  float K0 = 0.f, W[3][st::kMaxR + 1] = {};
+  float dtf = 0.f;
+  // scratch
+  Buf ac, p2, c2, tables;
+  Buf staging;       // pinned host staging for the src/rec tables
+  cudaEvent_t staging_ev = nullptr;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  bool broken = false;
+  std::string err;
+};
+
+namespace {
+
+st_status fail(stencil_plan* p, st_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (p) p->err = buf;
+  g_err = buf;
+  return s;
+}
+
+st_status cuda_fail(stencil_plan* p, cudaError_t e, const char* what) {
+  if (p && (e == cudaErrorIllegalAddress || e == cudaErrorLaunchFailure ||
+            e == cudaErrorIllegalInstruction || e == cudaErrorMisalignedAddress))
+    p->broken = true;
+  return fail(p, ST_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(p, _e, what); \
+  } while (0)
+
+long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+void free_buf(Buf& b) {
+  if (b.ptr) cudaFree(b.ptr);
+  b.ptr = nullptr;
+  b.bytes = 0;
+}
+
+st_status ensure_buf(stencil_plan* p, Buf& b, size_t bytes, const char* what) {
+  if (b.bytes >= bytes) return ST_OK;
+  free_buf(b);
+  cudaError_t e = cudaMalloc(&b.ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(p, ST_ENOMEM, "cudaMalloc(%zu) for %s failed: %s", bytes, what, cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  return ST_OK;
+}
+
+// ------------------------------------------------------------------ medium precompute (G0)
+// Per point (fp32, denormals flushed, no contraction; P:1678-1708 rewritten, see stencil.h):
+//   m = 1/(v*v); te = dt*eta; m2 = 2m; den = te + m2; a = (te - m2)/den; c = 2dt^2/den
+__device__ __forceinline__ float mul_ftz(float a, float b) { float r; asm("mul.rn.ftz.f32 %0,%1,%2;" : "=f"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ float add_ftz(float a, float b) { float r; asm("add.rn.ftz.f32 %0,%1,%2;" : "=f"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ float sub_ftz(float a, float b) { float r; asm("sub.rn.ftz.f32 %0,%1,%2;" : "=f"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ float div_ftz(float a, float b) { float r; asm("div.rn.ftz.f32 %0,%1,%2;" : "=f"(r) : "f"(a), "f"(b)); return r; }
+
+__device__ __forceinline__ void medium_point(float v, float eta, float dtf, float two_dt2, float& a, float& c) {
+  const float m = div_ftz(1.0f, mul_ftz(v, v));
+  const float te = mul_ftz(dtf, eta);
+  const float m2 = mul_ftz(2.0f, m);
+  const float den = add_ftz(te, m2);
+  a = div_ftz(sub_ftz(te, m2), den);
+  c = div_ftz(two_dt2, den);
+}
+
+__global__ void medium_kernel(const float* __restrict__ vel, const float* __restrict__ damp,
+                              float4* __restrict__ ac, int nx, int ny, long long X, long long plane,
+                              int z_lo, int nplanes, float dtf, float two_dt2) {
+  const long long X2 = X >> 1;
+  const long long per_plane = X2 * ny;
+  const long long total = per_plane * nplanes;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long z = z_lo + i / per_plane;
+    const long long rem = i % per_plane;
+    const long long y = rem / X2;
+    const long long xp = rem % X2;
+    const long long x = 2 * xp;
+    if (x >= nx) continue;
+    const long long off = z * plane + y * X + x;
+    const float2 v = *reinterpret_cast<const float2*>(vel + off);
+    float2 e = make_float2(0.f, 0.f);
+    if (damp) e = *reinterpret_cast<const float2*>(damp + off);
+    float a0, c0, a1 = 0.f, c1 = 0.f;
+    medium_point(v.x, e.x, dtf, two_dt2, a0, c0);
+    if (x + 1 < nx) medium_point(v.y, e.y, dtf, two_dt2, a1, c1);
+    ac[z * (plane >> 1) + y * X2 + xp] = make_float4(a0, a1, c0, c1);   // plane/2 float4 per plane
+  }
+}
+
+__global__ void swap_kernel(float4* __restrict__ a, float4* __restrict__ b, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 t = a[i];
+    a[i] = b[i];
+    b[i] = t;
+  }
+}
+
+// ------------------------------------------------------------------ tensor maps
+st_status encode_map(stencil_plan* p, const st::KernelEntry* k, const float* field, CUtensorMap* map) {
+  const long long zv_lo = p->G - (p->has_lo ? p->G : 0);
+  const long long zv_hi = p->G + p->nzl + (p->has_hi ? p->G : 0);
+  void* base = const_cast<float*>(field + zv_lo * p->X * p->Y);
+  cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)(zv_hi - zv_lo)};
+  cuuint64_t strides[2] = {(cuuint64_t)(p->X * 4), (cuuint64_t)(p->X * p->Y * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)k->bw, (cuuint32_t)k->bh, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = p->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(p, ST_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return ST_OK;
+}
+
+// choose ring depth / occupancy for one instance
+st_status configure_instance(stencil_plan* p, const st::KernelEntry* k, int* nslot, size_t* smem, int* bps) {
+  const size_t max_smem = 227 * 1024;
+  const int min_slots = k->rz + 2;
+  const int want_slots = k->rz + 1 + 3;      // prefetch depth 3 planes
+  int best_slots = 0, best_bps = 0;
+  size_t best_smem = 0;
+  for (int slots = std::max(min_slots, want_slots); slots >= min_slots; --slots) {
+    const size_t sm = k->fixed_bytes + (size_t)slots * k->slot_bytes;
+    if (sm > max_smem) continue;
+    int b = 0;
+    cudaError_t e = k->query(sm, nullptr, &b, k->nthreads);
+    if (e != cudaSuccess) return cuda_fail(p, e, "occupancy query");
+    if (b > best_bps || (b == best_bps && slots > best_slots)) {
+      best_bps = b; best_slots = slots; best_smem = sm;
+    }
+  }
+  if (best_slots == 0 || best_bps == 0)
+    return fail(p, ST_EUNSUPPORTED, "kernel instance (R=%d, T_k=%d) does not fit on this device", k->radius, k->tk);
+  // prefer two resident CTAs if a shallower ring allows it
+  *nslot = best_slots; *smem = best_smem; *bps = best_bps;
+  CK(k->query(best_smem, nullptr, nullptr, k->nthreads), "cudaFuncSetAttribute");
+  return ST_OK;
+}
+
+// ------------------------------------------------------------------ source/receiver tables
+struct Tables {
+  int nsrc_local = 0, nrec_local = 0;
+  size_t off_src_begin = 0, off_src = 0, off_rec_begin = 0, off_rec = 0, bytes = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+int32_t stencil_abi_version(void) { return 100; }
+
+int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel) {
+  return st::find_kernel(ndim, time_order, radius, t_kernel) != nullptr ? 1 : 0;
+}
+
+const char* stencil_last_error(const stencil_plan* p) {
+  if (p) return p->err.c_str();
+  return g_err.c_str();
+}
+
+st_status stencil_create(const st_config* cfg, stencil_plan** out) {
+  stencil_plan* p = nullptr;
+  if (!out) return fail(nullptr, ST_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, ST_EINVAL, "cfg is NULL");
+  const st_config& c = *cfg;
+  if (c.ndim != 2 && c.ndim != 3) return fail(nullptr, ST_EINVAL, "ndim must be 2 or 3 (got %d)", c.ndim);
+  if (c.radius < 1 || c.radius > st::kMaxR) return fail(nullptr, ST_EINVAL, "radius must be in 1..%d (got %d)", st::kMaxR, c.radius);
+  if (!c.coeffs) return fail(nullptr, ST_EINVAL, "coeffs is NULL");
+  if (c.time_order != 1 && c.time_order != 2) return fail(nullptr, ST_EINVAL, "time_order must be 1 or 2");
+  if (c.n[0] < 1 || c.n[1] < 1 || c.n[2] < 1) return fail(nullptr, ST_EINVAL, "grid sizes must be >= 1");
+  if (c.ndim == 2 && c.n[2] != 1) return fail(nullptr, ST_EINVAL, "2-D problems need n[2] == 1");
+  if (c.n[0] > (1ll << 30) || c.n[1] > (1ll << 30) || c.n[2] > (1ll << 30)) return fail(nullptr, ST_EINVAL, "grid too large");
+  if (c.t_kernel < 1) return fail(nullptr, ST_EINVAL, "t_kernel must be >= 1");
+  if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) return fail(nullptr, ST_EINVAL, "bad rank/nranks (%d/%d)", c.rank, c.nranks);
+  if (c.nranks > 1 && c.ndim != 3) return fail(nullptr, ST_EINVAL, "z-slab decomposition needs ndim == 3");
+  if (c.n[2] % c.nranks != 0) return fail(nullptr, ST_EINVAL, "n[2] %% nranks != 0");
+  if (c.nranks > 1 && (c.t_comm < 1 || c.t_comm % c.t_kernel != 0)) return fail(nullptr, ST_EINVAL, "t_comm must be a positive multiple of t_kernel");
+  if (!(c.dt > 0) || !(c.dx[0] > 0) || !(c.dx[1] > 0) || (c.ndim == 3 && !(c.dx[2] > 0))) return fail(nullptr, ST_EINVAL, "dt and dx must be positive");
+  if (!(c.flags & ST_FTZ)) return fail(nullptr, ST_EUNSUPPORTED, "only the flush-to-zero arithmetic mode is built (set ST_FTZ)");
+  const st::KernelEntry* ktk = st::find_kernel(c.ndim, c.time_order, c.radius, c.t_kernel);
+  const st::KernelEntry* kt1 = st::find_kernel(c.ndim, c.time_order, c.radius, 1);
+  if (!ktk || !kt1) return fail(nullptr, ST_EUNSUPPORTED, "no compiled kernel for ndim=%d time_order=%d radius=%d t_kernel=%d", c.ndim, c.time_order, c.radius, c.t_kernel);
+
+  p = new (std::nothrow) stencil_plan();
+  if (!p) return fail(nullptr, ST_ENOMEM, "host allocation failed");
+  p->cfg = c;
+  p->coeffs.assign(c.coeffs, c.coeffs + c.radius + 1);
+  p->cfg.coeffs = p->coeffs.data();
+  p->stream = static_cast<cudaStream_t>(c.stream);
+  p->device = c.device;
+  p->k_tk = ktk;
+  p->k_t1 = kt1;
+  auto bail = [&](st_status s) { std::string m = g_err; stencil_destroy(p); g_err = m; return s; };
+
+  cudaError_t e = cudaSetDevice(c.device);
+  if (e != cudaSuccess) { cuda_fail(p, e, "cudaSetDevice"); return bail(ST_ECUDA); }
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c.device);
+  cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, c.device);
+  if (major != 10) { fail(p, ST_EUNSUPPORTED, "device %d is not an sm_100 (Blackwell) GPU", c.device); return bail(ST_EUNSUPPORTED); }
+
+  // layout
+  p->nx = c.n[0]; p->ny = c.n[1];
+  p->nzl = (c.ndim == 3) ? c.n[2] / c.nranks : 1;
+  p->G = (c.nranks > 1) ? (long long)c.radius * c.t_comm : 0;
+  p->X = round_up(p->nx, 32);
+  p->Y = p->ny;
+  p->Z = p->nzl + 2 * p->G;
+  p->z0g = (long long)c.rank * p->nzl;
+  p->has_lo = c.rank > 0;
+  p->has_hi = c.rank < c.nranks - 1;
+
+  // coefficients (double, axes summed x, y, z; see stencil.h)
+  double k0 = 0.0;
+  for (int a = 0; a < c.ndim; ++a) k0 += p->coeffs[0] / (c.dx[a] * c.dx[a]);
+  p->K0 = (float)k0;
+  for (int a = 0; a < c.ndim; ++a)
+    for (int k = 1; k <= c.radius; ++k) p->W[a][k] = (float)(p->coeffs[k] / (c.dx[a] * c.dx[a]));
+  p->dtf = (float)c.dt;
+
+  // driver entry point for tensor-map encoding
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn) { cuda_fail(p, e == cudaSuccess ? cudaErrorNotSupported : e, "cuTensorMapEncodeTiled lookup"); return bail(ST_ECUDA); }
+  p->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+
+  st_status s = configure_instance(p, ktk, &p->nslot_tk, &p->smem_tk, &p->bps_tk);
+  if (s != ST_OK) return bail(s);
+  s = configure_instance(p, kt1, &p->nslot_t1, &p->smem_t1, &p->bps_t1);
+  if (s != ST_OK) return bail(s);
+
+  // scratch: medium (wave), ping-pong pair (t_kernel > 1)
+  const size_t field_bytes = (size_t)p->X * p->Y * p->Z * 4;
+  if (c.time_order == 2) {
+    s = ensure_buf(p, p->ac, 2 * field_bytes, "medium a/c");
+    if (s != ST_OK) return bail(s);
+  }
+  if (c.t_kernel > 1) {
+    s = ensure_buf(p, p->p2, field_bytes, "ping-pong u_prev");
+    if (s == ST_OK) s = ensure_buf(p, p->c2, field_bytes, "ping-pong u_cur");
+    if (s != ST_OK) return bail(s);
+  }
+  e = cudaEventCreateWithFlags(&p->staging_ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) { cuda_fail(p, e, "cudaEventCreate"); return bail(ST_ECUDA); }
+  *out = p;
+  return ST_OK;
+}
+
+st_status stencil_layout(const stencil_plan* p, int64_t padded[3], int64_t origin[3], int64_t zr[2]) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  if (padded) { padded[0] = p->X; padded[1] = p->Y; padded[2] = p->Z; }
+  if (origin) { origin[0] = 0; origin[1] = 0; origin[2] = p->G; }
+  if (zr) { zr[0] = p->z0g; zr[1] = p->z0g + p->nzl; }
+  return ST_OK;
+}
+
+void stencil_destroy(stencil_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  free_buf(p->ac); free_buf(p->p2); free_buf(p->c2); free_buf(p->tables);
+  if (p->staging.ptr) cudaFreeHost(p->staging.ptr);
+  if (p->staging_ev) cudaEventDestroy(p->staging_ev);
+  delete p;
+}
+
+st_status stencil_sync(stencil_plan* p) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  cudaSetDevice(p->device);
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) { p->broken = true; return cuda_fail(p, e, "stream synchronize"); }
+  return ST_OK;
+}
+
+static st_status upload_tables(stencil_plan* p, int32_t nsrc, const int32_t* src_xyz, int32_t nrec,
+                               const int32_t* rec_xyz, const int** src_begin, const int4** src,
+                               const int** rec_begin, const int4** rec) {
+  // sources: every plane of this slab's array (incl. ghosts) -> injected in redundant copies too
+  // receivers: owned planes only (unique writer per slab)
+  std::vector<int4> S, Rv;
+  const long long zlo_arr = p->G - (p->has_lo ? p->G : 0), zhi_arr = p->G + p->nzl + (p->has_hi ? p->G : 0);
+  for (int i = 0; i < nsrc; ++i) {
+    const long long z = (p->cfg.ndim == 3) ? src_xyz[3 * i + 2] - p->z0g + p->G : 0;
+    if (z >= zlo_arr && z < zhi_arr) S.push_back(make_int4(src_xyz[3 * i], src_xyz[3 * i + 1], (int)z, i));
+  }
+  for (int i = 0; i < nrec; ++i) {
+    const long long z = (p->cfg.ndim == 3) ? rec_xyz[3 * i + 2] - p->z0g + p->G : 0;
+    if (z >= p->G && z < p->G + p->nzl) Rv.push_back(make_int4(rec_xyz[3 * i], rec_xyz[3 * i + 1], (int)z, i));
+  }
+  auto by_plane = [](const int4& a, const int4& b) { return a.z < b.z; };
+  std::stable_sort(S.begin(), S.end(), by_plane);    // stable: index order within a point
+  std::stable_sort(Rv.begin(), Rv.end(), by_plane);
+  const int Zp1 = (int)p->Z + 1;
+  std::vector<int> sb(Zp1, 0), rb(Zp1, 0);
+  {
+    size_t i = 0;
+    for (int z = 0; z < Zp1; ++z) { while (i < S.size() && S[i].z < z) ++i; sb[z] = (int)i; }
+    i = 0;
+    for (int z = 0; z < Zp1; ++z) { while (i < Rv.size() && Rv[i].z < z) ++i; rb[z] = (int)i; }
+  }
+  const size_t b_sb = Zp1 * sizeof(int), b_s = std::max<size_t>(1, S.size()) * sizeof(int4);
+  const size_t b_rb = Zp1 * sizeof(int), b_r = std::max<size_t>(1, Rv.size()) * sizeof(int4);
+  const size_t o_s = round_up(b_sb, 16), o_rb = o_s + round_up(b_s, 16), o_r = o_rb + round_up(b_rb, 16);
+  const size_t total = o_r + b_r;
+  st_status s = ensure_buf(p, p->tables, total, "source/receiver tables");
+  if (s != ST_OK) return s;
+  if (p->staging.bytes < total) {
+    if (p->staging.ptr) { cudaEventSynchronize(p->staging_ev); cudaFreeHost(p->staging.ptr); }
+    p->staging.ptr = nullptr; p->staging.bytes = 0;
+    CK(cudaMallocHost(&p->staging.ptr, total), "cudaMallocHost");
+    p->staging.bytes = total;
+  } else {
+    CK(cudaEventSynchronize(p->staging_ev), "staging event");
+  }
+  char* h = static_cast<char*>(p->staging.ptr);
+  memcpy(h, sb.data(), b_sb);
+  if (!S.empty()) memcpy(h + o_s, S.data(), S.size() * sizeof(int4));
+  memcpy(h + o_rb, rb.data(), b_rb);
+  if (!Rv.empty()) memcpy(h + o_r, Rv.data(), Rv.size() * sizeof(int4));
+  CK(cudaMemcpyAsync(p->tables.ptr, h, total, cudaMemcpyHostToDevice, p->stream), "table upload");
+  CK(cudaEventRecord(p->staging_ev, p->stream), "staging event record");
+  char* d = static_cast<char*>(p->tables.ptr);
+  *src_begin = reinterpret_cast<const int*>(d);
+  *src = reinterpret_cast<const int4*>(d + o_s);
+  *rec_begin = reinterpret_cast<const int*>(d + o_rb);
+  *rec = reinterpret_cast<const int4*>(d + o_r);
+  return ST_OK;
+}
+
+static int choose_chunks(const stencil_plan* p, const st::KernelEntry* k, int bps, long long tiles, long long planes) {
+  const long long slots = (long long)p->sm_count * std::max(1, bps);
+  double best = 1e300;
+  int bestc = 1;
+  for (int c = 1; c <= 32; ++c) {
+    const long long chunk = (planes + c - 1) / c;
+    if (c > 1 && chunk < 8) break;
+    const long long ctas = tiles * c;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double per = (double)chunk + 2.0 * k->rz * k->tk;   // warm-up + redundant levels
+    const double t = waves * per;
+    if (t < best * 0.999) { best = t; bestc = c; }
+  }
+  return bestc;
+}
+
+st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
+                      const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
+                      const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
+                      const int32_t* rec_xyz, float* rec_trace) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  if (p->broken) return fail(p, ST_ESTATE, "plan is in an error state after an earlier CUDA fault");
+  const st_config& c = p->cfg;
+  const bool wave = c.time_order == 2;
+  if (!u_prev || !u_cur) return fail(p, ST_EINVAL, "u_prev/u_cur is NULL");
+  if (u_prev == u_cur) return fail(p, ST_EINVAL, "u_prev and u_cur must be distinct buffers");
+  if (wave && !vel) return fail(p, ST_EINVAL, "vel is NULL (wave)");
+  if (nt < 0) return fail(p, ST_EINVAL, "nt < 0");
+  if (step0 < 0) return fail(p, ST_EINVAL, "step0 < 0");
+  if (nsrc < 0 || nrec < 0) return fail(p, ST_EINVAL, "negative source/receiver count");
+  if (nsrc > 0 && (!src_xyz || !src_wavelet)) return fail(p, ST_EINVAL, "sources need src_xyz and src_wavelet");
+  if (nrec > 0 && (!rec_xyz || !rec_trace)) return fail(p, ST_EINVAL, "receivers need rec_xyz and rec_trace");
+  if (c.nranks > 1 && nt > c.t_comm) return fail(p, ST_EINVAL, "nt (%d) > t_comm (%d) with nranks > 1", nt, c.t_comm);
+  const long long nzg = c.n[2];
+  for (int i = 0; i < nsrc; ++i) {
+    const int32_t* q = src_xyz + 3 * i;
+    if (q[0] < 0 || q[0] >= c.n[0] || q[1] < 0 || q[1] >= c.n[1] || q[2] < 0 || q[2] >= nzg)
+      return fail(p, ST_EINVAL, "source %d (%d,%d,%d) outside the interior", i, q[0], q[1], q[2]);
+  }
+  for (int i = 0; i < nrec; ++i) {
+    const int32_t* q = rec_xyz + 3 * i;
+    if (q[0] < 0 || q[0] >= c.n[0] || q[1] < 0 || q[1] >= c.n[1] || q[2] < 0 || q[2] >= nzg)
+      return fail(p, ST_EINVAL, "receiver %d (%d,%d,%d) outside the interior", i, q[0], q[1], q[2]);
+  }
+  if (nt == 0) return ST_OK;
+  CK(cudaSetDevice(p->device), "cudaSetDevice");
+
+  const long long zv_lo = p->G - (p->has_lo ? p->G : 0);
+  const long long zv_hi = p->G + p->nzl + (p->has_hi ? p->G : 0);
+  const long long plane = p->X * p->Y;
+
+  // medium a/c over all valid planes
+  if (wave) {
+    const long long n = (p->X / 2) * p->Y * (zv_hi - zv_lo);
+    const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)p->sm_count * 16);
+    medium_kernel<<<blocks, 256, 0, p->stream>>>(vel, damp, static_cast<float4*>(p->ac.ptr), (int)p->nx, (int)p->ny,
+                                                  p->X, plane, (int)zv_lo, (int)(zv_hi - zv_lo), p->dtf,
+                                                  (float)(2.0 * c.dt * c.dt));
+    CK(cudaGetLastError(), "medium kernel launch");
+  }
+
+  const int *sbeg, *rbeg;
+  const int4 *sarr, *rarr;
+  st_status s = upload_tables(p, nsrc, src_xyz, nrec, rec_xyz, &sbeg, &sarr, &rbeg, &rarr);
+  if (s != ST_OK) return s;
+
+  // buffers: 0 = caller P, 1 = caller C, 2 = scratch P2, 3 = scratch C2
+  float* bufs[4] = {u_prev, u_cur, static_cast<float*>(p->p2.ptr), static_cast<float*>(p->c2.ptr)};
+  int prev = 0, cur = 1;
+  CUtensorMap maps_t1[4], maps_tk[4];
+  bool have_t1[4] = {false, false, false, false}, have_tk[4] = {false, false, false, false};
+
+  st::SweepParams sp{};
+  sp.nx = (int)p->nx; sp.ny = (int)p->ny; sp.X = (int)p->X; sp.plane = plane;
+  sp.gz_lo = p->has_lo ? 0 : (int)p->G;
+  sp.gz_hi = p->has_hi ? (int)p->Z : (int)(p->G + p->nzl);
+  sp.zv_lo = (int)zv_lo;
+  sp.ac = static_cast<const float4*>(p->ac.ptr);
+  sp.K0 = p->K0; sp.dt = p->dtf;
+  memcpy(sp.W, p->W, sizeof sp.W);
+  sp.src_begin = sbeg; sp.src = sarr; sp.wavelet = src_wavelet; sp.wl_stride = nsrc;
+  sp.rec_begin = rbeg; sp.rec = rarr; sp.trace = rec_trace; sp.tr_stride = nrec;
+
+  int j = 0;
+  while (j < nt) {
+    const bool tiled = (c.t_kernel > 1) && (nt - j >= c.t_kernel);
+    const int steps = tiled ? c.t_kernel : 1;
+    const st::KernelEntry* k = tiled ? p->k_tk : p->k_t1;
+    const int nslot = tiled ? p->nslot_tk : p->nslot_t1;
+    const size_t smem = tiled ? p->smem_tk : p->smem_t1;
+    const int bps = tiled ? p->bps_tk : p->bps_t1;
+    CUtensorMap* maps = tiled ? maps_tk : maps_t1;
+    bool* have = tiled ? have_tk : have_t1;
+    if (!have[cur]) {
+      s = encode_map(p, k, bufs[cur], &maps[cur]);
+      if (s != ST_OK) return s;
+      have[cur] = true;
+    }
+    // output plane range after j+steps of the nt steps covered by the ghost zones
+    const long long shrink = (long long)(nt - j - steps) * c.radius;
+    sp.out_lo = (int)(p->has_lo ? p->G - shrink : p->G);
+    sp.out_hi = (int)(p->has_hi ? p->G + p->nzl + shrink : p->G + p->nzl);
+    sp.P = bufs[prev];
+    int new_prev, new_cur;
+    if (!tiled) {
+      sp.outP = bufs[prev];            // in place: u^{n+1} over u^{n-1}
+      sp.outC = nullptr;
+      new_prev = cur; new_cur = prev;
+    } else {
+      const bool in_caller = prev < 2;
+      const int op = in_caller ? 2 : 0, oc = in_caller ? 3 : 1;
+      sp.outP = bufs[op];
+      sp.outC = bufs[oc];
+      new_prev = op; new_cur = oc;
+    }
+    sp.write_prev = (j + steps == nt) ? 1 : 0;
+    sp.wl_step = step0 + j;
+    sp.tr_step = j;
+    const long long tiles = ((p->nx + k->ox - 1) / k->ox) * ((p->ny + k->oy - 1) / k->oy);
+    const long long planes = sp.out_hi - sp.out_lo;
+    const int chunks = choose_chunks(p, k, bps, tiles, planes);
+    sp.zchunk = (int)((planes + chunks - 1) / chunks);
+    dim3 grid((unsigned)((p->nx + k->ox - 1) / k->ox), (unsigned)((p->ny + k->oy - 1) / k->oy), (unsigned)chunks);
+    CK(k->launch(maps[cur], sp, grid, nslot, smem, p->stream), "sweep kernel launch");
+    prev = new_prev; cur = new_cur;
+    j += steps;
+  }
+
+  // honour the contract: (u_prev, u_cur) buffers hold (u^{n+nt-1}, u^{n+nt})
+  const size_t field_bytes = (size_t)plane * p->Z * 4;
+  if (prev == 0 && cur == 1) {
+    // done
+  } else if (prev == 1 && cur == 0) {
+    const long long n4 = (long long)(field_bytes / 16);
+    const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)p->sm_count * 8);
+    swap_kernel<<<blocks, 256, 0, p->stream>>>(reinterpret_cast<float4*>(u_prev), reinterpret_cast<float4*>(u_cur), n4);
+    CK(cudaGetLastError(), "swap kernel launch");
+  } else {
+    CK(cudaMemcpyAsync(u_prev, bufs[prev], field_bytes, cudaMemcpyDeviceToDevice, p->stream), "copy u_prev");
+    CK(cudaMemcpyAsync(u_cur, bufs[cur], field_bytes, cudaMemcpyDeviceToDevice, p->stream), "copy u_cur");
+  }
+  return ST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// registry.h -- compiled kernel instances (one per (ndim, time_order, radius, t_kernel)).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstddef>
+
+#include "sweep.cuh"
+
+namespace st {
+
+typedef cudaError_t (*launch_fn)(const CUtensorMap& map, const SweepParams& p, dim3 grid,
+                                 int nslot, size_t smem, cudaStream_t stream);
+typedef cudaError_t (*attr_fn)(size_t smem, cudaFuncAttributes* attr, int* blocks_per_sm,
+                               int nthreads);
+
+struct KernelEntry {
+  int ndim, time_order, radius, tk;
+  int vy, nwy, nthreads;
+  int ox, oy;          // output tile
+  int bw, bh;          // TMA box
+  int rz;              // z radius (0 in 2-D)
+  size_t slot_bytes;   // one ring slot
+  size_t fixed_bytes;  // barriers + level buffers
+  launch_fn launch;
+  attr_fn query;       // sets max dynamic smem, returns attributes and occupancy
+};
+
+// Defined in the generated instance translation units.
+const KernelEntry* registry_begin();
+const KernelEntry* registry_end();
+const KernelEntry* find_kernel(int ndim, int time_order, int radius, int tk);
+
+template <int R, int TK, bool WAVE, int NDIM, int VY, int NWY>
+cudaError_t launch_sweep(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
+                         size_t smem, cudaStream_t stream) {
+  sweep_kernel<R, TK, WAVE, NDIM, VY, NWY><<<grid, 32 * NWY, smem, stream>>>(map, p, nslot);
+  return cudaGetLastError();
+}
+
+template <int R, int TK, bool WAVE, int NDIM, int VY, int NWY>
+cudaError_t query_sweep(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweep_kernel<R, TK, WAVE, NDIM, VY, NWY>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (attr) {
+    e = cudaFuncGetAttributes(attr, k);
+    if (e != cudaSuccess) return e;
+  }
+  if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, nthreads, smem);
+  return cudaSuccess;
+}
+
+template <int R, int TK, bool WAVE, int NDIM, int VY, int NWY>
+constexpr KernelEntry make_entry() {
+  using G = Geom<R, TK, NDIM, VY, NWY>;
+  return KernelEntry{NDIM, WAVE ? 2 : 1, R, TK, VY, NWY, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+                     G::RZ, (size_t)G::SLOT_BYTES,
+                     (size_t)128 + (TK > 1 ? (size_t)2 * (TK - 1) * G::LVL_FLOATS * 4 : 0),
+                     &launch_sweep<R, TK, WAVE, NDIM, VY, NWY>,
+                     &query_sweep<R, TK, WAVE, NDIM, VY, NWY>};
+}
+
+}  // namespace st

@@ -1,0 +1,143 @@
+"""Thin Python front end of libstencil.so: torch tensors for device memory and streams,
+ctypes for the C ABI (include/stencil.h).  Every step of the sweep runs in the CUDA library;
+this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .fd import fd_weights
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _points(pts) -> Tuple[int, Optional[np.ndarray]]:
+    if pts is None or len(pts) == 0:
+        return 0, None
+    a = np.ascontiguousarray(np.asarray(pts, dtype=np.int32).reshape(-1, 3))
+    return a.shape[0], a
+
+
+class Stencil:
+    """One plan: grid, stencil and time-tiling configuration on one CUDA device.
+
+    ndim: 2 or 3;  n: GLOBAL interior (nx, ny, nz);  space_order: 2..16 (radius = order/2);
+    time_order: 1 heat / 2 damped wave;  t_kernel: on-chip time-tile depth;  t_comm: halo depth
+    in steps for z-slabs (rank/nranks).  Layout: see include/stencil.h.
+    """
+
+    def __init__(self, ndim: int, n: Sequence[int], space_order: int, time_order: int, dt: float,
+                 dx: Sequence[float], t_kernel: int = 1, t_comm: int = 1, rank: int = 0,
+                 nranks: int = 1, device: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None,
+                 coeffs: Optional[Sequence[float]] = None):
+        lib = _lib.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.ndim, self.time_order, self.radius = ndim, time_order, space_order // 2
+        self.n = tuple(int(v) for v in n)
+        c = np.ascontiguousarray(fd_weights(space_order) if coeffs is None else coeffs, dtype=np.float64)
+        self._coeffs = c
+        cfg = _lib.StConfig()
+        cfg.ndim = ndim
+        cfg.n[:] = list(self.n)
+        cfg.radius = self.radius
+        cfg.coeffs = c.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        cfg.time_order = time_order
+        cfg.dt = float(dt)
+        dxs = list(dx) + [1.0] * (3 - len(dx))
+        cfg.dx[:] = [float(v) for v in dxs[:3]]
+        cfg.t_kernel, cfg.t_comm = int(t_kernel), int(t_comm)
+        cfg.rank, cfg.nranks = int(rank), int(nranks)
+        cfg.device = self.device
+        cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        cfg.flags = _lib.ST_FTZ
+        self._cfg = cfg
+        h = ctypes.c_void_p()
+        _lib.check(lib.stencil_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        padded = (ctypes.c_int64 * 3)()
+        origin = (ctypes.c_int64 * 3)()
+        zr = (ctypes.c_int64 * 2)()
+        _lib.check(lib.stencil_layout(h, padded, origin, zr), h)
+        self.X, self.Y, self.Z = padded[0], padded[1], padded[2]
+        self.G = origin[2]
+        self.z_range = (zr[0], zr[1])
+        self.t_kernel, self.t_comm, self.rank, self.nranks = t_kernel, t_comm, rank, nranks
+
+    # ------------------------------------------------------------------ layout helpers
+    @property
+    def shape(self):
+        return (self.Z, self.Y, self.X)
+
+    @property
+    def nz_local(self):
+        return self.z_range[1] - self.z_range[0]
+
+    def empty(self) -> torch.Tensor:
+        return torch.zeros(self.shape, dtype=torch.float32, device=f"cuda:{self.device}")
+
+    def embed(self, interior, ghost_lo: int = 0, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Place an interior array (planes, ny, nx) into the padded layout; its first plane goes
+        to array plane G - ghost_lo (so slabs with ghost planes can be embedded directly)."""
+        t = torch.as_tensor(interior)
+        out = self.empty() if out is None else out
+        z0 = self.G - ghost_lo
+        out[z0:z0 + t.shape[0], :, :self.n[0]].copy_(t, non_blocking=True)
+        return out
+
+    def interior(self, field: torch.Tensor) -> torch.Tensor:
+        """View of the owned interior (nz_local, ny, nx)."""
+        return field[self.G:self.G + (self.nz_local if self.ndim == 3 else 1), :, :self.n[0]]
+
+    # ------------------------------------------------------------------ run
+    def run(self, u_prev: torch.Tensor, u_cur: torch.Tensor, nt: int, vel: Optional[torch.Tensor] = None,
+            damp: Optional[torch.Tensor] = None, step0: int = 0, src=None,
+            wavelet: Optional[torch.Tensor] = None, rec=None,
+            trace: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+        """Advance (u_prev, u_cur) by nt steps in place (asynchronous on the plan's stream).
+        Returns the receiver trace tensor [nt, nrec] (allocated if not given)."""
+        for t in (u_prev, u_cur, vel, damp, wavelet, trace):
+            if t is not None:
+                if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+                    raise ValueError("fields/wavelet/trace must be contiguous float32 CUDA tensors")
+        for t in (u_prev, u_cur, vel, damp):
+            if t is not None and tuple(t.shape) != self.shape:
+                raise ValueError(f"field shape {tuple(t.shape)} != layout {self.shape}")
+        nsrc, src_a = _points(src)
+        nrec, rec_a = _points(rec)
+        if nrec and trace is None:
+            trace = torch.zeros((nt, nrec), dtype=torch.float32, device=u_cur.device)
+        lib = _lib.load()
+        st = lib.stencil_run(self._h, _ptr(u_prev), _ptr(u_cur), _ptr(vel), _ptr(damp), int(nt),
+                             int(step0), nsrc,
+                             None if src_a is None else src_a.ctypes.data_as(ctypes.c_void_p),
+                             _ptr(wavelet), nrec,
+                             None if rec_a is None else rec_a.ctypes.data_as(ctypes.c_void_p),
+                             _ptr(trace))
+        _lib.check(st, self._h)
+        return trace
+
+    def sync(self):
+        _lib.check(_lib.load().stencil_sync(self._h), self._h)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().stencil_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def supported(ndim: int, time_order: int, radius: int, t_kernel: int) -> bool:
+    return bool(_lib.load().stencil_supported(ndim, time_order, radius, t_kernel))
