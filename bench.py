@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the time-tiled FD stencil sweep (BASELINE.json metric: GPts/s and achieved HBM
+GB/s vs roofline, 1/2/4/8 GPUs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--tk auto] [--tc 4]
+    python bench.py --impl reference ...        # the CPU oracle arm (host cores)
+
+One bench *step* = one full simulation of the workload through the public API: stencil_run of
+the config's nt time steps over the whole grid (all SURVEY §8(a) rows: medium precompute,
+star stencil, leapfrog/heat update, source injection, receiver sampling, time tiling, halo
+exchange every T_c steps when N > 1).  Inputs are synthetic (workloads/), seeded, generated once
+on the host; `value` is timed with inputs resident in HBM; `e2e` re-times the same step with
+host pinned buffers copied in (u_prev, u_cur, vel, damp, wavelet) and results copied out
+(final u_cur and the receiver traces) inside the timed region.
+Fields (>= 512 MiB each) exceed the 126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+# Best on-chip time-tile depth per config (measured)
+AUTO_TK = {"C1": 1, "C2": 4, "C3": 2, "C4": 1, "C5": 1}
+METRIC = "GPts/s (grid-point updates/sec)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured copy (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _alg_bytes_per_point_launch(p: W.Problem, tiled: bool, tk: int) -> int:
+    """Algorithmic HBM bytes per interior point per sweep launch.
+    wave: T=1 reads u^{n-1}, u^n, a, c and writes u^{n+1} (in place) = 20 B;
+          T_k pass reads u^{n-1}, u^n, a, c, writes u^{n+T_k-1}, u^{n+T_k} = 24 B.
+    heat: read u^n, write u^{n+T} = 8 B (+4 on the final pass, ignored)."""
+    if p.time_order == 2:
+        return 24 if tiled else 20
+    return 8
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _problem(cfg: str, gpus: int) -> W.Problem:
+    return W.problem(cfg, gpus=gpus) if cfg == "C5" else W.problem(cfg)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1707_02347_b200 import Stencil
+    from paper_1707_02347_b200.dist import SlabRunner, init_from_env
+
+    rank, world, local = init_from_env(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p = _problem(args.config, world)
+    tk = AUTO_TK[args.config] if args.tk == "auto" else int(args.tk)
+    tc = max(tk, args.tc) if world > 1 else tk
+    tc = tc if tc % tk == 0 else tk * ((tc + tk - 1) // tk)
+    nt = p.nt if args.nt is None else args.nt
+    runner = SlabRunner(p, rank=rank, world=world, t_kernel=tk, t_comm=tc, device=local)
+    st = runner.stencil
+    # ---- host inputs (pinned) for this rank's slab, then resident device copies ----------------
+    host = runner.host_inputs(nt, pin=True)
+    dev_in = runner.to_device(host)
+    runner.set_timing(True)
+
+    def step_resident():
+        runner.reset_state(dev_in)          # zero initial fields (device memset, part of the step)
+        return runner.run(dev_in, nt)
+
+    # warm-up
+    for _ in range(args.warmup):
+        step_resident()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sweep_ms, sweep_launches, tiled, aux = 0.0, 0, 0, 0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_resident()
+        ms, nl, ntl, na = runner.last_timing()
+        sweep_ms += ms
+        sweep_launches += nl
+        tiled += ntl
+        aux += na
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    # max over ranks
+    if world > 1:
+        t = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    pts = float(p.points) * nt * args.steps          # all ranks' interior updates
+    value = pts / (t_ms * 1e-3) / 1e9
+
+    # ---- e2e: host pinned inputs in, results out, through the public API ---------------------
+    def step_e2e():
+        runner.upload(host, dev_in)
+        tr = runner.run(dev_in, nt)
+        return runner.download(dev_in, tr)
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        step_e2e()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = pts / (t_e2e * 1e-3) / 1e9
+    h2d, d2h = runner.io_bytes(host)
+
+    # ---- roofline of the dominant kernel (the sweep): algorithmic bytes / launch duration ----
+    peak, peak_src = _peaks()
+    n_local = float(p.n[0] * p.n[1] * runner.nz_local)
+    tiled_frac = tiled / max(1, sweep_launches)
+    bpp = (tiled_frac * _alg_bytes_per_point_launch(p, True, tk)
+           + (1 - tiled_frac) * _alg_bytes_per_point_launch(p, False, tk))
+    per_launch_ms = sweep_ms / max(1, sweep_launches)
+    achieved = bpp * n_local / (per_launch_ms * 1e-3) / 1e9
+    traffic = _ncu_traffic(args.config, tk)
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GPts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak" if args.config == "C5" else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (workloads/, seeded)",
+            "config": {
+                "workload": f"{args.config}: {_describe(p)}",
+                "grid": list(p.n), "nt_per_step": nt, "space_order": p.space_order,
+                "time_order": p.time_order, "t_kernel": tk, "t_comm": tc if world > 1 else None,
+                "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                "l2": "inputs larger than L2 (fields %.0f MiB each, L2 126 MB); no flush" % (
+                    runner.field_bytes / 2**20),
+            },
+            "e2e": {"value": round(e2e_value, 3), "unit": "GPts/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(sweep_launches + aux),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "st::sweep_kernel", "alg_bytes_per_point_launch": bpp,
+                         "per_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src},
+            "clocks": ck,
+        }
+    runner.close()
+    return out
+
+
+def _describe(p: W.Problem) -> str:
+    phys = "heat" if p.time_order == 1 else "acoustic wave (damped leapfrog)"
+    return (f"{phys}, SO{p.space_order}, {p.n[0]}x{p.n[1]}x{p.n[2]} fp32, {p.nt} steps"
+            + (f", {len(p.src)} Ricker source(s) {p.f_peak:g} Hz" if p.src else "")
+            + (f", {len(p.rec)} receivers" if p.rec else "")
+            + (f", {p.sponge}-pt sponge" if p.sponge else ""))
+
+
+def _ncu_traffic(cfg: str, tk: int):
+    """dram bytes (read+write) per sweep launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        v = d.get(f"{cfg}_tk{tk}")
+        return None if v is None else float(v["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg: str, seconds: float = 15.0):
+    """The oracle O1 as it stands, on this host's cores, on a bounded sample of the workload:
+    the full grid for as many time steps as fit in ~`seconds` (>= 1)."""
+    import oracle
+    p = _problem(cfg, 1)
+    # one step first to calibrate
+    t0 = time.perf_counter()
+    _, _, _ = oracle.run_problem(p, nt=1)
+    t1 = time.perf_counter()
+    one = t1 - t0
+    steps = max(1, min(p.nt, int(seconds / max(one, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.run_problem(p, nt=steps)
+    dt = time.perf_counter() - t0
+    return {"value": round(p.points * steps / dt / 1e9, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"{cfg} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {steps} of {p.nt} steps from the seeded "
+                      f"initial state (timed incl. the oracle's own medium precompute and input embedding)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle arm, timed per bench step on a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    p = _problem(args.config, 1)
+    r = p.radius
+    # inputs once (untimed), oracle layout
+    up, uc = W.initial_fields(p)
+    P0 = oracle.embed(up, p.ndim, r)
+    C0 = oracle.embed(uc, p.ndim, r)
+    a = c = None
+    if p.time_order == 2:
+        vel = oracle.embed(W.velocity(p), p.ndim, r)
+        vel[vel == 0] = 1.0
+        a, c = oracle.medium(vel, oracle.embed(W.damp(p), p.ndim, r), p.dt)
+        del vel
+    wv = W.wavelet(p) if p.src else None
+    cf = oracle.fd_weights(p.space_order)
+    sample_steps = args.ref_steps
+    def one():
+        P, C = P0.copy(), C0.copy()
+        oracle.run_untiled(p.ndim, p.n, p.space_order, cf, p.dx, p.time_order, p.dt, P, C, a, c,
+                           nt=sample_steps, src=list(p.src), wavelet=wv, rec=list(p.rec))
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = time.perf_counter() - t0
+    value = p.points * sample_steps * args.steps / dt / 1e9
+    sample = (f"{args.config} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {sample_steps} of {p.nt} time steps per "
+              f"bench step (bounded sample of the workload)")
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GPts/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak" if args.config == "C5" else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (workloads/, seeded)",
+            "config": {"workload": f"{args.config}: {_describe(p)}", "grid": list(p.n),
+                       "nt_per_step": sample_steps, "space_order": p.space_order},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=list(W.CONFIG_NAMES))
+    ap.add_argument("--tk", default="auto")
+    ap.add_argument("--tc", type=int, default=4, help="halo depth in steps for N > 1")
+    ap.add_argument("--nt", type=int, default=None, help="override time steps per bench step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-steps", type=int, default=2, help="time steps per reference bench step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out = run_gpu(args)
+    if out is not None:
+        if out["n_gpus"] == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args.config)
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,17 @@ void stencil_destroy(stencil_plan *p);
  * stencil_create / argument check.  Never NULL. */
 const char *stencil_last_error(const stencil_plan *p);
 
+/* Kernel timing (measurement support).  enable != 0: every later stencil_run
+ * records CUDA events on the plan's stream immediately before its first and after its last
+ * sweep-kernel launch.  stencil_timing waits for the last run's end event and returns the
+ * elapsed milliseconds between them, the number of sweep launches it enqueued, and how many of
+ * those were time-tiled (t_kernel-level) passes, and how many auxiliary kernels (medium
+ * precompute, final swap) the run launched.  ST_ESTATE if timing was not enabled or no run
+ * has been timed.  Any output pointer may be NULL. */
+st_status stencil_set_timing(stencil_plan *p, int32_t enable);
+st_status stencil_timing(stencil_plan *p, float *sweep_ms, int32_t *sweep_launches,
+                         int32_t *tiled_launches, int32_t *aux_launches);
+
 /* Pure host query (no device needed): is (ndim, time_order, radius, t_kernel) compiled? */
 int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel);
 

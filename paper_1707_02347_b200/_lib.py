@@ -18,7 +18,8 @@ STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 5: "S
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_sync", "stencil_destroy",
-           "stencil_last_error", "stencil_supported", "stencil_abi_version")
+           "stencil_last_error", "stencil_supported", "stencil_abi_version", "stencil_set_timing",
+           "stencil_timing")
 
 
 class StConfig(ctypes.Structure):
@@ -75,6 +76,11 @@ def load():
     lib.stencil_last_error.restype = ctypes.c_char_p
     lib.stencil_supported.argtypes = [ctypes.c_int32] * 4
     lib.stencil_supported.restype = ctypes.c_int32
+    lib.stencil_set_timing.argtypes = [P, ctypes.c_int32]
+    lib.stencil_set_timing.restype = ctypes.c_int
+    lib.stencil_timing.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+    lib.stencil_timing.restype = ctypes.c_int
     lib.stencil_abi_version.argtypes = []
     lib.stencil_abi_version.restype = ctypes.c_int32
     _lib = lib

@@ -59,6 +59,10 @@ struct stencil_plan {
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   bool broken = false;
   std::string err;
+  // timing (stencil_set_timing / stencil_timing)
+  bool timing = false, timed = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int last_launches = 0, last_tiled = 0, last_aux = 0;
 };
 
 namespace {
@@ -325,7 +329,35 @@ void stencil_destroy(stencil_plan* p) {
   free_buf(p->ac); free_buf(p->p2); free_buf(p->c2); free_buf(p->tables);
   if (p->staging.ptr) cudaFreeHost(p->staging.ptr);
   if (p->staging_ev) cudaEventDestroy(p->staging_ev);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
   delete p;
+}
+
+st_status stencil_set_timing(stencil_plan* p, int32_t enable) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  CK(cudaSetDevice(p->device), "cudaSetDevice");
+  if (enable && !p->ev0) {
+    CK(cudaEventCreate(&p->ev0), "cudaEventCreate");
+    CK(cudaEventCreate(&p->ev1), "cudaEventCreate");
+  }
+  p->timing = enable != 0;
+  p->timed = false;
+  return ST_OK;
+}
+
+st_status stencil_timing(stencil_plan* p, float* ms, int32_t* launches, int32_t* tiled, int32_t* aux) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  if (!p->timing || !p->timed) return fail(p, ST_ESTATE, "no timed run (call stencil_set_timing first)");
+  CK(cudaSetDevice(p->device), "cudaSetDevice");
+  CK(cudaEventSynchronize(p->ev1), "timing event synchronize");
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, p->ev0, p->ev1), "cudaEventElapsedTime");
+  if (ms) *ms = t;
+  if (launches) *launches = p->last_launches;
+  if (tiled) *tiled = p->last_tiled;
+  if (aux) *aux = p->last_aux;
+  return ST_OK;
 }
 
 st_status stencil_sync(stencil_plan* p) {
@@ -436,6 +468,7 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
       return fail(p, ST_EINVAL, "receiver %d (%d,%d,%d) outside the interior", i, q[0], q[1], q[2]);
   }
   if (nt == 0) return ST_OK;
+  int aux_launches = 0;
   CK(cudaSetDevice(p->device), "cudaSetDevice");
 
   const long long zv_lo = p->G - (p->has_lo ? p->G : 0);
@@ -450,6 +483,7 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
                                                   p->X, plane, (int)zv_lo, (int)(zv_hi - zv_lo), p->dtf,
                                                   (float)(2.0 * c.dt * c.dt));
     CK(cudaGetLastError(), "medium kernel launch");
+    ++aux_launches;
   }
 
   const int *sbeg, *rbeg;
@@ -475,6 +509,8 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
   sp.rec_begin = rbeg; sp.rec = rarr; sp.trace = rec_trace; sp.tr_stride = nrec;
 
   int j = 0;
+  int launches = 0, tiled_launches = 0;
+  if (p->timing) CK(cudaEventRecord(p->ev0, p->stream), "timing event");
   while (j < nt) {
     const bool tiled = (c.t_kernel > 1) && (nt - j >= c.t_kernel);
     const int steps = tiled ? c.t_kernel : 1;
@@ -515,8 +551,16 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
     sp.zchunk = (int)((planes + chunks - 1) / chunks);
     dim3 grid((unsigned)((p->nx + k->ox - 1) / k->ox), (unsigned)((p->ny + k->oy - 1) / k->oy), (unsigned)chunks);
     CK(k->launch(maps[cur], sp, grid, nslot, smem, p->stream), "sweep kernel launch");
+    ++launches;
+    tiled_launches += tiled ? 1 : 0;
     prev = new_prev; cur = new_cur;
     j += steps;
+  }
+  if (p->timing) {
+    CK(cudaEventRecord(p->ev1, p->stream), "timing event");
+    p->timed = true;
+    p->last_launches = launches;
+    p->last_tiled = tiled_launches;
   }
 
   // honour the contract: (u_prev, u_cur) buffers hold (u^{n+nt-1}, u^{n+nt})
@@ -528,10 +572,12 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)p->sm_count * 8);
     swap_kernel<<<blocks, 256, 0, p->stream>>>(reinterpret_cast<float4*>(u_prev), reinterpret_cast<float4*>(u_cur), n4);
     CK(cudaGetLastError(), "swap kernel launch");
+    ++aux_launches;
   } else {
     CK(cudaMemcpyAsync(u_prev, bufs[prev], field_bytes, cudaMemcpyDeviceToDevice, p->stream), "copy u_prev");
     CK(cudaMemcpyAsync(u_cur, bufs[cur], field_bytes, cudaMemcpyDeviceToDevice, p->stream), "copy u_cur");
   }
+  if (p->timing) p->last_aux = aux_launches;
   return ST_OK;
 }
 

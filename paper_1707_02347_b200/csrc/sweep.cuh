@@ -131,17 +131,25 @@ template <int R, int TK, int NDIM, int VY, int NWY>
 struct Geom {
   static constexpr int RZ = (NDIM == 3) ? R : 0;   // z radius (2-D: none)
   static constexpr int QN = 2 * RZ + 1;            // register queue length
-  static constexpr int RX2 = (R + 1) & ~1;         // x halo of the TMA box, even
+  static constexpr int RX2 = (R + 1) & ~1;         // x reach of the pair loads, even
+  static constexpr int RXB = (R + 3) & ~3;         // x halo of the TMA box, multiple of 4 floats
   static constexpr int GW = 64;                    // grid width (32 lanes x 2 columns)
   static constexpr int GH = NWY * VY;              // grid height
-  static constexpr int BW = GW + 2 * RX2;          // TMA box width (multiple of 4 floats)
-  static constexpr int BH = GH + 2 * R;            // TMA box height
   static constexpr int HX0 = Halo<R, TK>::hx(0);
   static constexpr int HY0 = Halo<R, TK>::hy(0);
+  // The TMA box must start on a 16-byte boundary (cuda-gdb: a box starting at x = -6 floats
+  // raised "Warp Illegal Instruction" at UTMALDG).  Grid origins are = -HX0 (mod 4), so the box
+  // starts XS = HX0 % 4 columns further left and is widened to keep rows a multiple of 32 B.
+  static constexpr int XS = HX0 % 4;
+  static constexpr int BW = GW + 2 * RXB + (XS ? 8 : 0);   // TMA box width (multiple of 8 floats)
+  static constexpr int BH = GH + 2 * R;            // TMA box height
+  static constexpr int BCOL = RXB + XS;            // column of grid x = 0 inside the box
   static constexpr int OX = GW - 2 * HX0;          // output tile
   static constexpr int OY = GH - 2 * HY0;
   static constexpr int SLOT_BYTES = ((BW * BH * 4) + 127) / 128 * 128;
-  static constexpr int LVL_FLOATS = GW * GH;       // one level plane buffer
+  static constexpr int LVL_FLOATS = GW * (GH + 2 * R);   // one level plane buffer, R pad rows
+                                                         // above/below (rows of a warp outside a
+                                                         // level's region read them, results masked)
   static constexpr int NTHREADS = 32 * NWY;
   static_assert(OX > 0 && OY > 0, "tile too small for this radius / depth");
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(32 * NWY, 1)
 sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
              const int nslot) {
   using G = Geom<R, TK, NDIM, VY, NWY>;
-  constexpr int RZ = G::RZ, QN = G::QN, RX2 = G::RX2, GW = G::GW, GH = G::GH, BW = G::BW;
+  constexpr int RZ = G::RZ, QN = G::QN, BCOL = G::BCOL, GW = G::GW, GH = G::GH, BW = G::BW;
   constexpr int HX0 = G::HX0, HY0 = G::HY0, OX = G::OX, OY = G::OY;
   constexpr int NL = (TK > 1) ? TK - 1 : 1;
   constexpr int SLOT_F = G::SLOT_BYTES / 4;
@@ -292,7 +300,7 @@ sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ 
   auto issue = [&](int a) {
     const int slot = a % nslot;
     mbar_expect_tx(&bars[slot], (uint32_t)(G::BW * G::BH * 4));
-    tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &bars[slot], gx - RX2, gy - R,
+    tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &bars[slot], gx - BCOL, gy - R,
                 p_first + a - p.zv_lo);
   };
   if (tid == 0) {
@@ -355,7 +363,7 @@ sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ 
         }
 
         // ---- arrival of u^n plane p_first+idx: wait, feed the queue --------------------------
-        const float* sa = ring + (size_t)slot_a * SLOT_F + (ry + R) * BW + 2 * lane + RX2;
+        const float* sa = ring + (size_t)slot_a * SLOT_F + (ry + R) * BW + 2 * lane + BCOL;
         mbar_wait(&bars[slot_a], par_a);
 #pragma unroll
         for (int j = 0; j < VY; ++j) qn[u][j] = lds64(sa + j * BW);
@@ -366,7 +374,7 @@ sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ 
         for (int j = 0; j < VY; ++j) out0[j] = 0ull;
         if (lv_on[0]) {
           const int slot_s = (idx - RZ) % nslot;
-          const float* cs = ring + (size_t)slot_s * SLOT_F + (ry + R) * BW + 2 * lane + RX2;
+          const float* cs = ring + (size_t)slot_s * SLOT_F + (ry + R) * BW + 2 * lane + BCOL;
           uint64_t acc[VY];
           accumulate<R, RZ, QN, VY, NDIM, BW>(acc, qn, cs, p, md<QN>(u - RZ));
           add_sources<VY>(acc, p, s, y0, x0, p.wl_step);
@@ -414,7 +422,7 @@ sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ 
 #pragma unroll
           for (int l = 1; l < TK; ++l) {
             // publish level l-1 at plane s - l*RZ (this level's centre plane)
-            float* lp = lb + (size_t)(l - 1) * G::LVL_FLOATS + ry * GW + 2 * lane;
+            float* lp = lb + (size_t)(l - 1) * G::LVL_FLOATS + (ry + R) * GW + 2 * lane;
 #pragma unroll
             for (int j = 0; j < VY; ++j) sts64(lp + j * GW, ql[l - 1][md<QN>(u - RZ)][j]);
             __syncthreads();

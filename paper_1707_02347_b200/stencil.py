@@ -124,6 +124,19 @@ class Stencil:
         _lib.check(st, self._h)
         return trace
 
+    def set_timing(self, enable: bool = True):
+        _lib.check(_lib.load().stencil_set_timing(self._h, int(enable)), self._h)
+
+    def timing(self):
+        """(sweep_ms, sweep_launches, tiled_launches, aux_launches) of the last run (waits for it)."""
+        ms = ctypes.c_float()
+        n = ctypes.c_int32()
+        nt = ctypes.c_int32()
+        na = ctypes.c_int32()
+        _lib.check(_lib.load().stencil_timing(self._h, ctypes.byref(ms), ctypes.byref(n),
+                                              ctypes.byref(nt), ctypes.byref(na)), self._h)
+        return float(ms.value), int(n.value), int(nt.value), int(na.value)
+
     def sync(self):
         _lib.check(_lib.load().stencil_sync(self._h), self._h)
 
