@@ -30,8 +30,13 @@ def _vy_nwy(ndim: int, R: int, TK: int):
     return 2, 12
 
 
+NCW_T1 = 16   # consumer warps (= tile rows) of the untiled warp-specialised kernel
+
+
 def instances():
-    """(ndim, wave, R, TK, VY, NWY) compiled into this build."""
+    """(ndim, wave, R, TK, VY, NWY) compiled into this build.
+    TK == 1 entries use the warp-specialised untiled kernel (sweep1.cuh, NCW_T1 rows),
+    TK > 1 the temporally blocked kernel (sweep.cuh)."""
     out = []
     for wave in (0, 1):
         for R in range(1, 9):
@@ -54,7 +59,11 @@ def _gen_sources(groups: int):
     for gi, group in enumerate(per):
         lines = ['#include "registry.h"', "namespace st {", f"extern const KernelEntry kInst{gi}[] = {{"]
         for (ndim, wave, R, TK, VY, NWY) in group:
-            lines.append(f"  make_entry<{R}, {TK}, {'true' if wave else 'false'}, {ndim}, {VY}, {NWY}>(),")
+            w = 'true' if wave else 'false'
+            if TK == 1:
+                lines.append(f"  make_entry1<{R}, {w}, {ndim}, {NCW_T1}>(),")
+            else:
+                lines.append(f"  make_entry<{R}, {TK}, {w}, {ndim}, {VY}, {NWY}>(),")
         lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]
         files.append((os.path.join(BUILD, f"inst_{gi}.cu"), "\n".join(lines)))
     reg = ['#include "registry.h"', "#include <vector>", "namespace st {"]
@@ -91,7 +100,8 @@ def _digest(paths):
 
 def _compile(src: str, log: bool):
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "registry.h"),
+    deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "sweep1.cuh"),
+            os.path.join(CSRC, "registry.h"),
             os.path.join(HERE, "..", "include", "stencil.h")]
     stamp = obj + ".stamp"
     d = _digest(deps)

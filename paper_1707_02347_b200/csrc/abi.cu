@@ -183,7 +183,7 @@ st_status encode_map(stencil_plan* p, const st::KernelEntry* k, const float* fie
 st_status configure_instance(stencil_plan* p, const st::KernelEntry* k, int* nslot, size_t* smem, int* bps) {
   const size_t max_smem = 227 * 1024;
   const int min_slots = k->rz + 2;
-  const int want_slots = k->rz + 1 + 3;      // prefetch depth 3 planes
+  const int want_slots = std::min(64, k->rz + 1 + k->extra_depth);   // prefetch depth in planes
   int best_slots = 0, best_bps = 0;
   size_t best_smem = 0;
   for (int slots = std::max(min_slots, want_slots); slots >= min_slots; --slots) {
@@ -243,6 +243,9 @@ st_status stencil_create(const st_config* cfg, stencil_plan** out) {
   if (c.nranks > 1 && c.ndim != 3) return fail(nullptr, ST_EINVAL, "z-slab decomposition needs ndim == 3");
   if (c.n[2] % c.nranks != 0) return fail(nullptr, ST_EINVAL, "n[2] %% nranks != 0");
   if (c.nranks > 1 && (c.t_comm < 1 || c.t_comm % c.t_kernel != 0)) return fail(nullptr, ST_EINVAL, "t_comm must be a positive multiple of t_kernel");
+  if (c.nranks > 1 && (long long)c.radius * c.t_comm > c.n[2] / c.nranks)
+    return fail(nullptr, ST_EINVAL, "ghost depth radius*t_comm (%lld) exceeds the slab thickness (%lld planes)",
+                (long long)c.radius * c.t_comm, (long long)(c.n[2] / c.nranks));
   if (!(c.dt > 0) || !(c.dx[0] > 0) || !(c.dx[1] > 0) || (c.ndim == 3 && !(c.dx[2] > 0))) return fail(nullptr, ST_EINVAL, "dt and dx must be positive");
   if (!(c.flags & ST_FTZ)) return fail(nullptr, ST_EUNSUPPORTED, "only the flush-to-zero arithmetic mode is built (set ST_FTZ)");
   const st::KernelEntry* ktk = st::find_kernel(c.ndim, c.time_order, c.radius, c.t_kernel);

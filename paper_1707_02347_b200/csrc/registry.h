@@ -5,6 +5,7 @@
 #include <cstddef>
 
 #include "sweep.cuh"
+#include "sweep1.cuh"
 
 namespace st {
 
@@ -23,6 +24,7 @@ struct KernelEntry {
   size_t fixed_bytes;  // barriers + level buffers
   launch_fn launch;
   attr_fn query;       // sets max dynamic smem, returns attributes and occupancy
+  int extra_depth;     // preferred ring prefetch depth beyond the rz+1 resident planes
 };
 
 // Defined in the generated instance translation units.
@@ -57,7 +59,36 @@ constexpr KernelEntry make_entry() {
                      G::RZ, (size_t)G::SLOT_BYTES,
                      (size_t)128 + (TK > 1 ? (size_t)2 * (TK - 1) * G::LVL_FLOATS * 4 : 0),
                      &launch_sweep<R, TK, WAVE, NDIM, VY, NWY>,
-                     &query_sweep<R, TK, WAVE, NDIM, VY, NWY>};
+                     &query_sweep<R, TK, WAVE, NDIM, VY, NWY>, 3};
+}
+
+// ---- warp-specialised untiled kernel (sweep1.cuh)
+template <int R, bool WAVE, int NDIM, int NCW>
+cudaError_t launch_sweep1(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
+                          size_t smem, cudaStream_t stream) {
+  sweep1_kernel<R, WAVE, NDIM, NCW><<<grid, 32 * (NCW + 1), smem, stream>>>(map, p, nslot);
+  return cudaGetLastError();
+}
+
+template <int R, bool WAVE, int NDIM, int NCW>
+cudaError_t query_sweep1(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweep1_kernel<R, WAVE, NDIM, NCW>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (attr) {
+    e = cudaFuncGetAttributes(attr, k);
+    if (e != cudaSuccess) return e;
+  }
+  if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, nthreads, smem);
+  return cudaSuccess;
+}
+
+template <int R, bool WAVE, int NDIM, int NCW>
+constexpr KernelEntry make_entry1() {
+  using G = Geom1<R, NDIM, NCW>;
+  return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, 1, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+                     G::RZ, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
+                     &launch_sweep1<R, WAVE, NDIM, NCW>, &query_sweep1<R, WAVE, NDIM, NCW>, 6};
 }
 
 }  // namespace st

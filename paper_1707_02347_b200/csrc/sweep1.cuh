@@ -1,0 +1,246 @@
+// sweep1.cuh -- untiled (one time level per pass) 2.5-D sweep for sm_100a, warp-specialised.
+//
+// The T=1 member of the schedule family (Devito's space-only blocking; SURVEY §8
+// row a2/a3).  One CTA = one x-y tile of 64 x NCW points streaming z:
+//   * warp NCW (producer): one elected lane issues the TMA load of every u^n plane box
+//     (tile + radius halo, OOB zero-filled = Dirichlet) into a ring of NSLOT shared-memory slots,
+//     waiting on the slot's EMPTY mbarrier before reuse and arming its FULL mbarrier;
+//   * warps 0..NCW-1 (consumers): warp w owns row w of the tile, a column PAIR per lane (packed
+//     fp32x2 math).  Each keeps its own z-column of 2r+1 planes in registers, reads x/y
+//     neighbours from the ring slot of the centre plane, computes u^{n+1} in the canonical order
+//     (include/stencil.h), stores it in place over u^{n-1}, and releases the slot (EMPTY arrive).
+// Consumers never synchronise with each other, so warps drift within the ring depth and HBM
+// latency hides behind the other warps' work; u^{n-1} and the medium (a, c) are staged PD planes
+// ahead into per-warp shared memory with cp.async (LDGSTS) and waited for with wait_group, so no
+// register ever waits on a fresh load.  The body is unrolled by the queue length only (one row per
+// warp) and carries no per-step division, 64-bit index math or table lookups, which keeps the
+// loop small (instruction-cache resident) and the issue slots for the stencil arithmetic.
+#pragma once
+#include "sweep.cuh"
+
+namespace st {
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async8(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float4* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// Rare paths kept out of the unrolled body (called only by warps whose row holds an event).
+static __device__ __noinline__ uint64_t add_sources_row(uint64_t acc, const SweepParams& p, int s, int y,
+                                                 int x0, long long wl_step) {
+  const int sb = __ldg(p.src_begin + s), se = __ldg(p.src_begin + s + 1);
+  for (int i = sb; i < se; ++i) {
+    const int4 e = __ldg(p.src + i);
+    if (e.y == y && (e.x == x0 || e.x == x0 + 1)) {
+      const float w = __ldg(p.wavelet + wl_step * p.wl_stride + e.w);
+      acc = (e.x == x0) ? pack2(fadd_ftz(lo_of(acc), w), hi_of(acc))
+                        : pack2(lo_of(acc), fadd_ftz(hi_of(acc), w));
+    }
+  }
+  return acc;
+}
+static __device__ __noinline__ void sample_receivers_row(uint64_t o, const SweepParams& p, int s, int y,
+                                                  int x0, int tr_step) {
+  const int rb = __ldg(p.rec_begin + s), re = __ldg(p.rec_begin + s + 1);
+  for (int i = rb; i < re; ++i) {
+    const int4 e = __ldg(p.rec + i);
+    if (e.y == y && (e.x == x0 || e.x == x0 + 1))
+      p.trace[(long long)tr_step * p.tr_stride + e.w] = (e.x == x0) ? lo_of(o) : hi_of(o);
+  }
+}
+
+template <int R, int NDIM, int NCW>
+struct Geom1 {
+  static constexpr int RZ = (NDIM == 3) ? R : 0;
+  static constexpr int QN = 2 * RZ + 1;
+  static constexpr int RX2 = (R + 1) & ~1;
+  static constexpr int RXB = (R + 3) & ~3;         // box x halo, multiple of 4 floats (16 B)
+  static constexpr int GW = 64, GH = NCW;
+  static constexpr int BW = GW + 2 * RXB;          // multiple of 8 floats
+  static constexpr int BH = GH + 2 * R;
+  static constexpr int OX = GW, OY = GH;
+  static constexpr int SLOT_BYTES = ((BW * BH * 4) + 127) / 128 * 128;
+  static constexpr int NTHREADS = 32 * (NCW + 1);
+  static constexpr int PD = 4;                     // cp.async staging distance (planes)
+  static constexpr int STAGE_F = 64 + 128;         // one staged plane row: u^{n-1} (64) + {a,c} (128)
+  static constexpr int STAGE_BYTES = NCW * (PD + 1) * STAGE_F * 4;
+  static_assert(BW <= 256 && BH <= 256, "TMA box limit");
+};
+
+// Is any table entry (sorted by plane) on planes [z0, z1) in row y, columns [x0, x1)?
+__device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent, int z0, int z1,
+                                              int y, int x0, int x1) {
+  const int b = __ldg(begin + z0), e = __ldg(begin + z1);
+  for (int i = b; i < e; ++i) {
+    const int4 t = __ldg(ent + i);
+    if (t.y == y && t.x >= x0 && t.x < x1) return true;
+  }
+  return false;
+}
+
+template <int R, bool WAVE, int NDIM, int NCW>
+__global__ void __launch_bounds__(32 * (NCW + 1), 1)
+sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
+              const int nslot) {
+  using G = Geom1<R, NDIM, NCW>;
+  constexpr int RZ = G::RZ, QN = G::QN, RX2 = G::RX2, RXB = G::RXB, BW = G::BW;
+  constexpr int SLOT_F = G::SLOT_BYTES / 4;
+  constexpr int PD = G::PD, STAGE_F = G::STAGE_F;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + nslot;
+  float* ring = reinterpret_cast<float*>(smem + ((16 * nslot + 127) / 128) * 128);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int tx0 = blockIdx.x * G::OX, ty0 = blockIdx.y * G::OY;
+  const int zb = p.out_lo + blockIdx.z * p.zchunk;
+  const int ze = min(p.out_hi, zb + p.zchunk);
+  if (zb >= ze) return;
+  const int p_first = zb - RZ;
+  const int n_arr = (ze - 1 + RZ) - p_first + 1;
+
+  if (tid == 0) {
+    for (int i = 0; i < nslot; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 32 * NCW);   // every consumer lane arrives
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ------------------------------------------------------------------ producer warp
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmapC)) : "memory");
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int a = 0; a < n_arr; ++a) {
+        if (a >= nslot) mbar_wait(&empty[slot], ph ^ 1u);
+        mbar_expect_tx(&full[slot], (uint32_t)(BW * G::BH * 4));
+        tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &full[slot], tx0 - RXB, ty0 - R,
+                    p_first + a - p.zv_lo);
+        if (++slot == nslot) { slot = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumer warps
+  const int x0 = tx0 + 2 * lane;
+  const int y = ty0 + warp;
+  const bool xin0 = x0 < p.nx, xin1 = x0 + 1 < p.nx;
+  const bool yin = y < p.ny;                      // warp-uniform
+  const bool act = yin && xin0;                   // this lane owns >= 1 interior point
+  const uint64_t mask = yin ? ((xin0 ? 0xffffffffull : 0ull) | (xin1 ? 0xffffffff00000000ull : 0ull)) : 0ull;
+  const int col = (warp + R) * BW + 2 * lane + RXB;   // my pair in a ring slot
+  const uint64_t K0 = splat(p.K0);
+  const uint64_t DT = splat(p.dt);
+  // planes [clo, chi) are computed (the rest of [zb, ze) is global halo -> untouched)
+  const int clo = max(zb, p.gz_lo), chi = min(ze, p.gz_hi);
+  // rare events of this warp's row (sources / receivers), decided once per CTA chunk
+  const bool wsrc = yin && row_has_entry(p.src_begin, p.src, zb, ze, y, tx0, tx0 + 64);
+  const bool wrec = yin && row_has_entry(p.rec_begin, p.rec, zb, ze, y, tx0, tx0 + 64);
+
+  // u^{n-1} and the medium {a,a,c,c} of plane s are staged into per-warp shared memory with
+  // cp.async PD planes ahead (no registers held across steps, no wait on fresh loads).
+  const long long plane = p.plane;
+  float* stage = ring + (size_t)nslot * SLOT_F + (size_t)warp * (PD + 1) * STAGE_F;
+  const int s0 = zb - 2 * RZ;                       // level-0 plane of arrival 0
+  const float* gP = p.P + (long long)s0 * plane + (long long)y * p.X + x0;
+  const float4* gA = p.ac + (long long)s0 * (plane >> 1) + (long long)y * (p.X >> 1) + (x0 >> 1);
+  float* out = p.outP + (long long)s0 * plane + (long long)y * p.X + x0;
+  int e_use = 0, e_iss = 0;                         // staging entries of plane s and of s + PD
+  auto stage_plane = [&](int q, int e) {            // issue the copies of plane q into entry e
+    if (WAVE && act && q >= clo && q < chi) {
+      const long long dq = (long long)(q - s0);
+      cp_async8(stage + e * STAGE_F + 2 * lane, gP + dq * plane);
+      cp_async16(stage + e * STAGE_F + 64 + 4 * lane, gA + dq * (plane >> 1));
+    }
+    cp_async_commit();
+  };
+  if (WAVE) {
+#pragma unroll 1
+    for (int i = 0; i < PD; ++i) { stage_plane(s0 + i, e_iss); if (++e_iss == PD + 1) e_iss = 0; }
+  }
+
+  uint64_t qn[QN];
+#pragma unroll
+  for (int i = 0; i < QN; ++i) qn[i] = 0ull;
+  int slot_a = 0, slot_s = RZ % nslot; // ring slots of the arriving plane and of the centre plane
+                                       // (the first centre, plane zb, is arrival RZ)
+  uint32_t ph_a = 0;
+
+  for (int base = 0; base < n_arr; base += QN) {
+#pragma unroll
+    for (int u = 0; u < QN; ++u) {
+      const int idx = base + u;
+      if (idx < n_arr) {
+        const int s = s0 + idx;
+        if (WAVE) { stage_plane(s + PD, e_iss); if (++e_iss == PD + 1) e_iss = 0; }
+
+        mbar_wait(&full[slot_a], ph_a);
+        const float* sa = ring + slot_a * SLOT_F;
+        qn[u] = lds64(sa + col);
+        if (idx < RZ || idx >= n_arr - RZ) mbar_arrive(&empty[slot_a]);   // never a centre plane
+        if (idx >= 2 * RZ) {                      // step s in [zb, ze)
+          if (s >= clo && s < chi && act) {
+            const float* rp = ring + slot_s * SLOT_F + col;
+            const uint64_t c = qn[md<QN>(u - RZ)];
+            uint64_t A[RX2 + 1];
+#pragma unroll
+            for (int m = -RX2 / 2; m <= RX2 / 2; ++m) A[m + RX2 / 2] = (m == 0) ? c : lds64(rp + 2 * m);
+            uint64_t acc = f2mul(K0, c);
+#pragma unroll
+            for (int k = 1; k <= R; ++k) {
+              uint64_t sx;
+              if ((k & 1) == 0) {
+                sx = f2add(A[RX2 / 2 - k / 2], A[RX2 / 2 + k / 2]);
+              } else {
+                const uint64_t Lm = A[RX2 / 2 - (k + 1) / 2], L0 = A[RX2 / 2 - (k - 1) / 2];
+                const uint64_t R0 = A[RX2 / 2 + (k - 1) / 2], Rp = A[RX2 / 2 + (k + 1) / 2];
+                sx = pack2(fadd_ftz(hi_of(Lm), hi_of(R0)), fadd_ftz(lo_of(L0), lo_of(Rp)));
+              }
+              acc = f2fma(splat(p.W[0][k]), sx, acc);
+              acc = f2fma(splat(p.W[1][k]), f2add(lds64(rp - k * BW), lds64(rp + k * BW)), acc);
+              if (NDIM == 3)
+                acc = f2fma(splat(p.W[2][k]), f2add(qn[md<QN>(u - RZ - k)], qn[md<QN>(u - RZ + k)]), acc);
+            }
+            if (wsrc) acc = add_sources_row(acc, p, s, y, x0, p.wl_step);
+            uint64_t o;
+            if (WAVE) {
+              cp_async_wait<PD>();                 // the group of plane s has landed
+              const float* st_e = stage + e_use * STAGE_F;
+              const uint64_t pv = lds64(st_e + 2 * lane);
+              const float4 m4 = *reinterpret_cast<const float4*>(st_e + 64 + 4 * lane);
+              o = f2fma(pack2(m4.z, m4.w), acc, f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c));
+            } else {
+              o = f2fma(DT, acc, c);
+            }
+            o &= mask;
+            if (xin1) sts64(out, o);
+            else *out = lo_of(o);
+            if (wrec) sample_receivers_row(o, p, s, y, x0, p.tr_step);
+          }
+          mbar_arrive(&empty[slot_s]);
+          if (++slot_s == nslot) slot_s = 0;
+        }
+        if (WAVE && ++e_use == PD + 1) e_use = 0;
+        out += plane;
+        if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
+      }
+    }
+  }
+  if (WAVE) cp_async_wait<0>();
+}
+
+}  // namespace st

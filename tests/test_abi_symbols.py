@@ -76,6 +76,7 @@ def _cfg(**kw):
     (dict(nranks=2, n=[16, 16, 15]), _lib.ST_EINVAL),
     (dict(nranks=2, rank=2), _lib.ST_EINVAL),
     (dict(nranks=2, t_kernel=2, t_comm=3), _lib.ST_EINVAL),
+    (dict(nranks=4, t_comm=5), _lib.ST_EINVAL),              # ghost depth 5 > slab of 4 planes
     (dict(flags=0), _lib.ST_EUNSUPPORTED),
     (dict(radius=3, t_kernel=8), _lib.ST_EUNSUPPORTED),
 ])

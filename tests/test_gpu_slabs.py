@@ -61,14 +61,24 @@ def _run_slabs(p, world, tk, tc):
     return P, C, T
 
 
-@pytest.mark.parametrize("world,tk,tc", [(2, 1, 1), (2, 1, 3), (3, 2, 2), (4, 2, 4), (2, 2, 6), (4, 1, 4)])
+@pytest.mark.parametrize("world,tk,tc", [(2, 1, 1), (2, 1, 3), (3, 2, 2), (4, 2, 2), (2, 2, 6), (4, 1, 3),
+                                          (8, 1, 1)])
 def test_emulated_slabs_bitwise(world, tk, tc):
-    p = _problem()
+    p = _problem(nz=64 if world == 8 else 48)
     got = _run_slabs(p, world, tk, tc)
     want = oracle.run_problem(p)
     assert np.abs(want[1]).max() > 0
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
+
+
+def test_ghost_deeper_than_slab_rejected():
+    from paper_1707_02347_b200 import Stencil
+    from paper_1707_02347_b200._lib import ST_EINVAL, StencilError
+    p = _problem()
+    with pytest.raises(StencilError) as e:
+        Stencil(3, p.n, 8, 2, p.dt, p.dx, t_kernel=1, t_comm=4, rank=0, nranks=4)   # 16 > 12 planes
+    assert e.value.status == ST_EINVAL
 
 
 @pytest.mark.parametrize("order", [2, 12, 16])
