@@ -102,8 +102,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
   do {
+    // suspend-time hint: the warp sleeps in hardware until the phase completes (no spin issue)
     asm volatile("{\n\t.reg .pred q;\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 0x989680;\n\t"
                  "selp.u32 %0, 1, 0, q;\n\t}"
                  : "=r"(ok) : "r"(a), "r"(parity) : "memory");
   } while (!ok);

@@ -145,32 +145,33 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   const int col = (warp + R) * BW + 2 * lane + RXB;   // my pair in a ring slot
   const uint64_t K0 = splat(p.K0);
   const uint64_t DT = splat(p.dt);
-  // planes [clo, chi) are computed (the rest of [zb, ze) is global halo -> untouched)
-  const int clo = max(zb, p.gz_lo), chi = min(ze, p.gz_hi);
   // rare events of this warp's row (sources / receivers), decided once per CTA chunk
   const bool wsrc = yin && row_has_entry(p.src_begin, p.src, zb, ze, y, tx0, tx0 + 64);
   const bool wrec = yin && row_has_entry(p.rec_begin, p.rec, zb, ze, y, tx0, tx0 + 64);
 
   // u^{n-1} and the medium {a,a,c,c} of plane s are staged into per-warp shared memory with
   // cp.async PD planes ahead (no registers held across steps, no wait on fresh loads).
+  // Every plane of [zb, ze) lies inside the global domain (host invariant), so each step computes.
   const long long plane = p.plane;
   float* stage = ring + (size_t)nslot * SLOT_F + (size_t)warp * (PD + 1) * STAGE_F;
   const int s0 = zb - 2 * RZ;                       // level-0 plane of arrival 0
-  const float* gP = p.P + (long long)s0 * plane + (long long)y * p.X + x0;
-  const float4* gA = p.ac + (long long)s0 * (plane >> 1) + (long long)y * (p.X >> 1) + (x0 >> 1);
-  float* out = p.outP + (long long)s0 * plane + (long long)y * p.X + x0;
-  int e_use = 0, e_iss = 0;                         // staging entries of plane s and of s + PD
-  auto stage_plane = [&](int q, int e) {            // issue the copies of plane q into entry e
-    if (WAVE && act && q >= clo && q < chi) {
-      const long long dq = (long long)(q - s0);
-      cp_async8(stage + e * STAGE_F + 2 * lane, gP + dq * plane);
-      cp_async16(stage + e * STAGE_F + 64 + 4 * lane, gA + dq * (plane >> 1));
+  const float* gP = p.P + (long long)zb * plane + (long long)y * p.X + x0;   // plane zb
+  const float4* gA = p.ac + (long long)zb * (plane >> 1) + (long long)y * (p.X >> 1) + (x0 >> 1);
+  float* out = p.outP + (long long)zb * plane + (long long)y * p.X + x0;
+  int q_iss = zb;                                   // next plane to stage
+  int e_use = 0, e_iss = 0;                         // staging entries of plane s and of q_iss
+  auto stage_next = [&]() {                         // stage plane q_iss (if in the chunk)
+    if (q_iss < ze && act) {
+      cp_async8(stage + e_iss * STAGE_F + 2 * lane, gP);
+      cp_async16(stage + e_iss * STAGE_F + 64 + 4 * lane, gA);
     }
     cp_async_commit();
+    gP += plane; gA += plane >> 1; ++q_iss;
+    if (++e_iss == PD + 1) e_iss = 0;
   };
   if (WAVE) {
 #pragma unroll 1
-    for (int i = 0; i < PD; ++i) { stage_plane(s0 + i, e_iss); if (++e_iss == PD + 1) e_iss = 0; }
+    for (int i = 0; i < PD; ++i) stage_next();
   }
 
   uint64_t qn[QN];
@@ -185,57 +186,55 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     for (int u = 0; u < QN; ++u) {
       const int idx = base + u;
       if (idx < n_arr) {
-        const int s = s0 + idx;
-        if (WAVE) { stage_plane(s + PD, e_iss); if (++e_iss == PD + 1) e_iss = 0; }
-
         mbar_wait(&full[slot_a], ph_a);
-        const float* sa = ring + slot_a * SLOT_F;
-        qn[u] = lds64(sa + col);
-        if (idx < RZ || idx >= n_arr - RZ) mbar_arrive(&empty[slot_a]);   // never a centre plane
-        if (idx >= 2 * RZ) {                      // step s in [zb, ze)
-          if (s >= clo && s < chi && act) {
-            const float* rp = ring + slot_s * SLOT_F + col;
-            const uint64_t c = qn[md<QN>(u - RZ)];
-            uint64_t A[RX2 + 1];
+        qn[u] = lds64(ring + slot_a * SLOT_F + col);
+        if (idx < RZ) mbar_arrive(&empty[slot_a]);   // planes below zb are never a centre
+        if (idx >= 2 * RZ) {                          // step s = s0 + idx in [zb, ze)
+          if (WAVE) stage_next();                     // plane s + PD
+          const int s = s0 + idx;
+          const float* rp = ring + slot_s * SLOT_F + col;
+          const uint64_t c = qn[md<QN>(u - RZ)];
+          uint64_t A[RX2 + 1];
 #pragma unroll
-            for (int m = -RX2 / 2; m <= RX2 / 2; ++m) A[m + RX2 / 2] = (m == 0) ? c : lds64(rp + 2 * m);
-            uint64_t acc = f2mul(K0, c);
+          for (int m = -RX2 / 2; m <= RX2 / 2; ++m) A[m + RX2 / 2] = (m == 0) ? c : lds64(rp + 2 * m);
+          uint64_t acc = f2mul(K0, c);
 #pragma unroll
-            for (int k = 1; k <= R; ++k) {
-              uint64_t sx;
-              if ((k & 1) == 0) {
-                sx = f2add(A[RX2 / 2 - k / 2], A[RX2 / 2 + k / 2]);
-              } else {
-                const uint64_t Lm = A[RX2 / 2 - (k + 1) / 2], L0 = A[RX2 / 2 - (k - 1) / 2];
-                const uint64_t R0 = A[RX2 / 2 + (k - 1) / 2], Rp = A[RX2 / 2 + (k + 1) / 2];
-                sx = pack2(fadd_ftz(hi_of(Lm), hi_of(R0)), fadd_ftz(lo_of(L0), lo_of(Rp)));
-              }
-              acc = f2fma(splat(p.W[0][k]), sx, acc);
-              acc = f2fma(splat(p.W[1][k]), f2add(lds64(rp - k * BW), lds64(rp + k * BW)), acc);
-              if (NDIM == 3)
-                acc = f2fma(splat(p.W[2][k]), f2add(qn[md<QN>(u - RZ - k)], qn[md<QN>(u - RZ + k)]), acc);
-            }
-            if (wsrc) acc = add_sources_row(acc, p, s, y, x0, p.wl_step);
-            uint64_t o;
-            if (WAVE) {
-              cp_async_wait<PD>();                 // the group of plane s has landed
-              const float* st_e = stage + e_use * STAGE_F;
-              const uint64_t pv = lds64(st_e + 2 * lane);
-              const float4 m4 = *reinterpret_cast<const float4*>(st_e + 64 + 4 * lane);
-              o = f2fma(pack2(m4.z, m4.w), acc, f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c));
+          for (int k = 1; k <= R; ++k) {
+            uint64_t sx;
+            if ((k & 1) == 0) {
+              sx = f2add(A[RX2 / 2 - k / 2], A[RX2 / 2 + k / 2]);
             } else {
-              o = f2fma(DT, acc, c);
+              const uint64_t Lm = A[RX2 / 2 - (k + 1) / 2], L0 = A[RX2 / 2 - (k - 1) / 2];
+              const uint64_t R0 = A[RX2 / 2 + (k - 1) / 2], Rp = A[RX2 / 2 + (k + 1) / 2];
+              sx = pack2(fadd_ftz(hi_of(Lm), hi_of(R0)), fadd_ftz(lo_of(L0), lo_of(Rp)));
             }
-            o &= mask;
+            acc = f2fma(splat(p.W[0][k]), sx, acc);
+            acc = f2fma(splat(p.W[1][k]), f2add(lds64(rp - k * BW), lds64(rp + k * BW)), acc);
+            if (NDIM == 3)
+              acc = f2fma(splat(p.W[2][k]), f2add(qn[md<QN>(u - RZ - k)], qn[md<QN>(u - RZ + k)]), acc);
+          }
+          if (wsrc) acc = add_sources_row(acc, p, s, y, x0, p.wl_step);
+          uint64_t o;
+          if (WAVE) {
+            cp_async_wait<PD>();                      // the group of plane s has landed
+            const float* st_e = stage + e_use * STAGE_F;
+            const uint64_t pv = lds64(st_e + 2 * lane);
+            const float4 m4 = *reinterpret_cast<const float4*>(st_e + 64 + 4 * lane);
+            o = f2fma(pack2(m4.z, m4.w), acc, f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c));
+            if (++e_use == PD + 1) e_use = 0;
+          } else {
+            o = f2fma(DT, acc, c);
+          }
+          o &= mask;
+          if (act) {
             if (xin1) sts64(out, o);
             else *out = lo_of(o);
-            if (wrec) sample_receivers_row(o, p, s, y, x0, p.tr_step);
           }
+          if (wrec) sample_receivers_row(o, p, s, y, x0, p.tr_step);
           mbar_arrive(&empty[slot_s]);
           if (++slot_s == nslot) slot_s = 0;
+          out += plane;
         }
-        if (WAVE && ++e_use == PD + 1) e_use = 0;
-        out += plane;
         if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
       }
     }
