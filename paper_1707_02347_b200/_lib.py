@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstencil.so")
+LIB_PATH = os.environ.get("ST_LIB") or os.path.join(HERE, "libstencil.so")   # ST_LIB: experiment builds
 
 ST_OK, ST_EINVAL, ST_ENOMEM, ST_ECUDA, ST_EUNSUPPORTED, ST_ESTATE = 0, 1, 2, 3, 5, 6
 ST_FTZ = 1

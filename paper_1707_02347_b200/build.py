@@ -51,9 +51,10 @@ def instances():
     return out
 
 
-def _gen_sources(groups: int):
-    os.makedirs(BUILD, exist_ok=True)
-    inst = instances()
+def _gen_sources(groups: int, inst=None, outdir: str = BUILD, ncw: int = NCW_T1):
+    os.makedirs(outdir, exist_ok=True)
+    inst = instances() if inst is None else inst
+    groups = max(1, min(groups, len(inst)))
     files = []
     per = [inst[i::groups] for i in range(groups)]
     for gi, group in enumerate(per):
@@ -61,11 +62,11 @@ def _gen_sources(groups: int):
         for (ndim, wave, R, TK, VY, NWY) in group:
             w = 'true' if wave else 'false'
             if TK == 1:
-                lines.append(f"  make_entry1<{R}, {w}, {ndim}, {NCW_T1}>(),")
+                lines.append(f"  make_entry1<{R}, {w}, {ndim}, {ncw}>(),")
             else:
                 lines.append(f"  make_entry<{R}, {TK}, {w}, {ndim}, {VY}, {NWY}>(),")
         lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]
-        files.append((os.path.join(BUILD, f"inst_{gi}.cu"), "\n".join(lines)))
+        files.append((os.path.join(outdir, f"inst_{gi}.cu"), "\n".join(lines)))
     reg = ['#include "registry.h"', "#include <vector>", "namespace st {"]
     for gi in range(groups):
         reg.append(f"extern const KernelEntry kInst{gi}[]; extern const int kInst{gi}Count;")
@@ -81,7 +82,7 @@ def _gen_sources(groups: int):
                "    if (e.ndim == ndim && e.time_order == time_order && e.radius == radius && e.tk == tk) return &e;\n"
                "  return nullptr;\n}")
     reg += ["}  // namespace st", ""]
-    files.append((os.path.join(BUILD, "registry.cu"), "\n".join(reg)))
+    files.append((os.path.join(outdir, "registry.cu"), "\n".join(reg)))
     for path, text in files:
         if not os.path.exists(path) or open(path).read() != text:
             with open(path, "w") as f:
@@ -89,25 +90,25 @@ def _gen_sources(groups: int):
     return [f for f, _ in files]
 
 
-def _digest(paths):
+def _digest(paths, extra=()):
     h = hashlib.sha256()
     for pth in sorted(paths):
         with open(pth, "rb") as f:
             h.update(f.read())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + FLAGS + list(extra)).encode())
     return h.hexdigest()[:16]
 
 
-def _compile(src: str, log: bool):
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src: str, outdir: str = BUILD, defines=()):
+    obj = os.path.join(outdir, os.path.basename(src) + ".o")
     deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "sweep1.cuh"),
             os.path.join(CSRC, "registry.h"),
             os.path.join(HERE, "..", "include", "stencil.h")]
     stamp = obj + ".stamp"
-    d = _digest(deps)
+    d = _digest(deps, defines)
     if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == d:
         return obj, ""
-    cmd = [NVCC] + ARCH + FLAGS + ["-I", CSRC, "-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + FLAGS + list(defines) + ["-I", CSRC, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-6000:]}")
@@ -116,30 +117,43 @@ def _compile(src: str, log: bool):
     return obj, r.stderr
 
 
-def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
-    groups = 12
-    srcs = _gen_sources(groups) + [os.path.join(CSRC, "abi.cu")]
-    if force:
-        for s in srcs:
-            o = os.path.join(BUILD, os.path.basename(s) + ".o")
-            if os.path.exists(o):
-                os.remove(o)
+def _build(outdir, lib, inst=None, defines=(), groups=12, jobs=0, verbose=False, ncw=NCW_T1):
+    srcs = _gen_sources(groups, inst, outdir, ncw) + [os.path.join(CSRC, "abi.cu")]
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     objs, logs = [], []
     with cf.ThreadPoolExecutor(jobs) as ex:
-        for obj, log in ex.map(lambda s: _compile(s, verbose), srcs):
+        for obj, log in ex.map(lambda s: _compile(s, outdir, defines), srcs):
             objs.append(obj)
             logs.append(log)
     if verbose:
-        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        with open(os.path.join(outdir, "ptxas.log"), "w") as f:
             f.write("\n".join(logs))
-    need = force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)
+    need = not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs)
     if need:
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    return LIB
+    return lib
+
+
+def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
+    if force and os.path.isdir(BUILD):
+        for f in os.listdir(BUILD):
+            if f.endswith(".o") or f.endswith(".stamp"):
+                os.remove(os.path.join(BUILD, f))
+    return _build(BUILD, LIB, jobs=jobs, verbose=verbose)
+
+
+def build_variant(name: str, defines=(), only=None, ncw: int = NCW_T1, verbose: bool = True) -> str:
+    """Experimental library _variants/libstencil_<name>.so with extra -D flags and (optionally)
+    only the instances whose (ndim, wave, R, TK) is listed; load it with ST_LIB=<path>."""
+    inst = instances()
+    if only is not None:
+        inst = [i for i in inst if tuple(i[:4]) in set(map(tuple, only))]
+    outdir = os.path.join(HERE, "_variants", name)
+    lib = os.path.join(HERE, "_variants", f"libstencil_{name}.so")
+    return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose, ncw=ncw)
 
 
 if __name__ == "__main__":

@@ -7,6 +7,10 @@
 #include "sweep.cuh"
 #include "sweep1.cuh"
 
+#ifndef ST_T1_DEPTH
+#define ST_T1_DEPTH 6   // untiled kernel: ring planes of prefetch beyond the radius+1 in use
+#endif
+
 namespace st {
 
 typedef cudaError_t (*launch_fn)(const CUtensorMap& map, const SweepParams& p, dim3 grid,
@@ -88,7 +92,7 @@ constexpr KernelEntry make_entry1() {
   using G = Geom1<R, NDIM, NCW>;
   return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, 1, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      G::RZ, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
-                     &launch_sweep1<R, WAVE, NDIM, NCW>, &query_sweep1<R, WAVE, NDIM, NCW>, 6};
+                     &launch_sweep1<R, WAVE, NDIM, NCW>, &query_sweep1<R, WAVE, NDIM, NCW>, ST_T1_DEPTH};
 }
 
 }  // namespace st

@@ -69,7 +69,10 @@ struct Geom1 {
   static constexpr int OX = GW, OY = GH;
   static constexpr int SLOT_BYTES = ((BW * BH * 4) + 127) / 128 * 128;
   static constexpr int NTHREADS = 32 * (NCW + 1);
-  static constexpr int PD = 4;                     // cp.async staging distance (planes)
+#ifndef ST_PD
+#define ST_PD 4
+#endif
+  static constexpr int PD = ST_PD;                 // cp.async staging distance (planes)
   static constexpr int STAGE_F = 64 + 128;         // one staged plane row: u^{n-1} (64) + {a,c} (128)
   static constexpr int STAGE_BYTES = NCW * (PD + 1) * STAGE_F * 4;
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
