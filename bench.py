@@ -33,7 +33,7 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 # Best on-chip time-tile depth per config (measured)
-AUTO_TK = {"C1": 1, "C2": 4, "C3": 2, "C4": 1, "C5": 1}
+AUTO_TK = {"C1": 1, "C2": 4, "C3": 1, "C4": 1, "C5": 1}
 METRIC = "GPts/s (grid-point updates/sec)"
 
 
@@ -73,6 +73,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()            # wait for the first sample so the timed region is covered
+            while not self.lines and time.time() - t0 < 10:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
 
@@ -251,35 +254,11 @@ def _ncu_traffic(cfg: str, tk: int):
         return None
 
 
-def cpu_baseline(cfg: str, seconds: float = 15.0):
-    """The oracle O1 as it stands, on this host's cores, on a bounded sample of the workload:
-    the full grid for as many time steps as fit in ~`seconds` (>= 1)."""
+def _oracle_inputs(cfg: str):
+    """The oracle's own inputs for the config (untimed): embedded fields, medium, wavelet."""
     import oracle
     p = _problem(cfg, 1)
-    # one step first to calibrate
-    t0 = time.perf_counter()
-    _, _, _ = oracle.run_problem(p, nt=1)
-    t1 = time.perf_counter()
-    one = t1 - t0
-    steps = max(1, min(p.nt, int(seconds / max(one, 1e-3))))
-    t0 = time.perf_counter()
-    oracle.run_problem(p, nt=steps)
-    dt = time.perf_counter() - t0
-    return {"value": round(p.points * steps / dt / 1e9, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
-            "kind": "oracle",
-            "sample": f"{cfg} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {steps} of {p.nt} steps from the seeded "
-                      f"initial state (timed incl. the oracle's own medium precompute and input embedding)"}
-
-
-def run_reference(args):
-    """--impl reference: the CPU oracle arm, timed per bench step on a bounded sample."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return None
-    import oracle
-    p = _problem(args.config, 1)
     r = p.radius
-    # inputs once (untimed), oracle layout
     up, uc = W.initial_fields(p)
     P0 = oracle.embed(up, p.ndim, r)
     C0 = oracle.embed(uc, p.ndim, r)
@@ -290,12 +269,49 @@ def run_reference(args):
         a, c = oracle.medium(vel, oracle.embed(W.damp(p), p.ndim, r), p.dt)
         del vel
     wv = W.wavelet(p) if p.src else None
-    cf = oracle.fd_weights(p.space_order)
+    return p, P0, C0, a, c, wv
+
+
+def _oracle_steps(p, P0, C0, a, c, wv, nt):
+    """O1 as it stands: nt time steps of the full grid from the initial state."""
+    import oracle
+    P, C = P0.copy(), C0.copy()
+    oracle.run_untiled(p.ndim, p.n, p.space_order, oracle.fd_weights(p.space_order), p.dx,
+                       p.time_order, p.dt, P, C, a, c, nt=nt, src=list(p.src), wavelet=wv,
+                       rec=list(p.rec))
+
+
+def cpu_baseline(cfg: str, seconds: float = 15.0):
+    """The oracle O1 as it stands, on this host's cores, on a bounded sample of the workload:
+    the full grid for as many time steps as fit in ~`seconds` (>= 1); input generation untimed."""
+    import oracle
+    ins = _oracle_inputs(cfg)
+    p = ins[0]
+    t0 = time.perf_counter()
+    _oracle_steps(*ins, nt=1)                      # calibration step
+    one = time.perf_counter() - t0
+    steps = max(1, min(p.nt, int(seconds / max(one, 1e-3))))
+    t0 = time.perf_counter()
+    _oracle_steps(*ins, nt=steps)
+    dt = time.perf_counter() - t0
+    return {"value": round(p.points * steps / dt / 1e9, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"{cfg} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {steps} of {p.nt} time steps from the "
+                      f"seeded initial state (O1 loop nest only; input generation untimed)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle arm, timed per bench step on a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    ins = _oracle_inputs(args.config)
+    p = ins[0]
     sample_steps = args.ref_steps
+
     def one():
-        P, C = P0.copy(), C0.copy()
-        oracle.run_untiled(p.ndim, p.n, p.space_order, cf, p.dx, p.time_order, p.dt, P, C, a, c,
-                           nt=sample_steps, src=list(p.src), wavelet=wv, rec=list(p.rec))
+        _oracle_steps(*ins, nt=sample_steps)
     for _ in range(args.warmup):
         one()
     t0 = time.perf_counter()
