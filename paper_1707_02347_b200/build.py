@@ -22,7 +22,8 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 
 def _vy_nwy(ndim: int, R: int, TK: int):
-    """Register blocking per instance: queues hold TK*(2R+1)*VY packed pairs per thread."""
+    """Register blocking of the first time-tiled kernel (sweep.cuh): queues hold TK*(2R+1)*VY
+    packed pairs per thread."""
     if ndim == 2:
         return 4, 8
     if TK * (2 * R + 1) * 4 <= 72:
@@ -32,22 +33,39 @@ def _vy_nwy(ndim: int, R: int, TK: int):
 
 NCW_T1 = 16   # consumer warps (= tile rows) of the untiled warp-specialised kernel
 
+# kernel kinds: 1 = sweep1 (untiled, warp-specialised), 2 = sweep2 (time-tiled, warp-specialised),
+#               0 = sweep (first time-tiled kernel; 2-D and the shapes sweep2 does not fit)
+T2_GEOM = {2: (11, 2), 1: (15, 2)}   # time_order -> (consumer warps NCW, rows per warp VY)
+
+
+def _sweep2_fits(wave: int, R: int, TK: int) -> bool:
+    if wave:
+        return TK == 2 and R <= 4
+    return (R == 1 and TK in (2, 4)) or (R == 2 and TK in (2, 4))
+
 
 def instances():
-    """(ndim, wave, R, TK, VY, NWY) compiled into this build.
-    TK == 1 entries use the warp-specialised untiled kernel (sweep1.cuh, NCW_T1 rows),
-    TK > 1 the temporally blocked kernel (sweep.cuh)."""
+    """(ndim, wave, R, TK, VY, NWY, kind) compiled into this build."""
     out = []
     for wave in (0, 1):
+        to = 2 if wave else 1
         for R in range(1, 9):
-            for TK in (1, 2):
-                out.append((3, wave, R, TK) + _vy_nwy(3, R, TK))
+            out.append((3, wave, R, 1, 1, NCW_T1, 1))
+            if _sweep2_fits(wave, R, 2):
+                ncw, vy = T2_GEOM[to]
+                out.append((3, wave, R, 2, vy, ncw, 2))
+            else:
+                out.append((3, wave, R, 2) + _vy_nwy(3, R, 2) + (0,))
         for R in range(1, 9):
-            out.append((2, wave, R, 1) + _vy_nwy(2, R, 1))
-        out.append((2, wave, 1, 2) + _vy_nwy(2, 1, 2))
-        out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4))
+            out.append((2, wave, R, 1, 1, NCW_T1, 1))
+        out.append((2, wave, 1, 2) + _vy_nwy(2, 1, 2) + (0,))
+        out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4) + (0,))
     for R, TK in ((1, 4), (2, 4), (1, 8)):
-        out.append((3, 0, R, TK) + _vy_nwy(3, R, TK))
+        if _sweep2_fits(0, R, TK):
+            ncw, vy = T2_GEOM[1]
+            out.append((3, 0, R, TK, vy, ncw, 2))
+        else:
+            out.append((3, 0, R, TK) + _vy_nwy(3, R, TK) + (0,))
     return out
 
 
@@ -59,10 +77,12 @@ def _gen_sources(groups: int, inst=None, outdir: str = BUILD, ncw: int = NCW_T1)
     per = [inst[i::groups] for i in range(groups)]
     for gi, group in enumerate(per):
         lines = ['#include "registry.h"', "namespace st {", f"extern const KernelEntry kInst{gi}[] = {{"]
-        for (ndim, wave, R, TK, VY, NWY) in group:
+        for (ndim, wave, R, TK, VY, NWY, kind) in group:
             w = 'true' if wave else 'false'
-            if TK == 1:
+            if kind == 1:
                 lines.append(f"  make_entry1<{R}, {w}, {ndim}, {ncw}>(),")
+            elif kind == 2:
+                lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}, {VY}>(),")
             else:
                 lines.append(f"  make_entry<{R}, {TK}, {w}, {ndim}, {VY}, {NWY}>(),")
         lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]
@@ -102,6 +122,7 @@ def _digest(paths, extra=()):
 def _compile(src: str, outdir: str = BUILD, defines=()):
     obj = os.path.join(outdir, os.path.basename(src) + ".o")
     deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "sweep1.cuh"),
+            os.path.join(CSRC, "sweep2.cuh"),
             os.path.join(CSRC, "registry.h"),
             os.path.join(HERE, "..", "include", "stencil.h")]
     stamp = obj + ".stamp"

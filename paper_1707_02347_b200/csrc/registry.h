@@ -6,6 +6,7 @@
 
 #include "sweep.cuh"
 #include "sweep1.cuh"
+#include "sweep2.cuh"
 
 #ifndef ST_T1_DEPTH
 #define ST_T1_DEPTH 6   // untiled kernel: ring planes of prefetch beyond the radius+1 in use
@@ -93,6 +94,40 @@ constexpr KernelEntry make_entry1() {
   return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, 1, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      G::RZ, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
                      &launch_sweep1<R, WAVE, NDIM, NCW>, &query_sweep1<R, WAVE, NDIM, NCW>, ST_T1_DEPTH};
+}
+
+// ---- warp-specialised time-tiled kernel (sweep2.cuh)
+template <int R, int TK, bool WAVE, int NCW, int VY>
+cudaError_t launch_sweep2(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
+                          size_t smem, cudaStream_t stream) {
+  sweep2_kernel<R, TK, WAVE, NCW, VY><<<grid, 32 * (NCW + 1), smem, stream>>>(map, p, nslot);
+  return cudaGetLastError();
+}
+
+template <int R, int TK, bool WAVE, int NCW, int VY>
+cudaError_t query_sweep2(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweep2_kernel<R, TK, WAVE, NCW, VY>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (attr) {
+    e = cudaFuncGetAttributes(attr, k);
+    if (e != cudaSuccess) return e;
+  }
+  if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, nthreads, smem);
+  return cudaSuccess;
+}
+
+#ifndef ST_T2_DEPTH
+#define ST_T2_DEPTH 3   // time-tiled kernel: ring planes of prefetch beyond the radius+1 in use
+#endif
+
+template <int R, int TK, bool WAVE, int NCW, int VY>
+constexpr KernelEntry make_entry2() {
+  using G = Geom2<R, TK, WAVE, NCW, VY>;
+  return KernelEntry{3, WAVE ? 2 : 1, R, TK, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+                     R, (size_t)G::SLOT_BYTES, (size_t)G::FIXED_BYTES,
+                     &launch_sweep2<R, TK, WAVE, NCW, VY>, &query_sweep2<R, TK, WAVE, NCW, VY>,
+                     ST_T2_DEPTH};
 }
 
 }  // namespace st

@@ -43,7 +43,7 @@ def main():
         print("RESULT", json.dumps({"cfg": a.child, "bitwise": ok}))
         return
     from paper_1707_02347_b200.build import instances
-    cfgs = [(nd, 2 * R, 2 if w else 1, TK) for (nd, w, R, TK, _, _) in instances()]
+    cfgs = [(nd, 2 * R, 2 if w else 1, TK) for (nd, w, R, TK, *_rest) in instances()]
     if a.only:
         cfgs = [tuple(map(int, a.only.split(",")))]
     for c in cfgs:
