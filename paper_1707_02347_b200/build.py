@@ -35,25 +35,26 @@ NCW_T1 = 16   # consumer warps (= tile rows) of the untiled warp-specialised ker
 
 # kernel kinds: 1 = sweep1 (untiled, warp-specialised), 2 = sweep2 (time-tiled, warp-specialised),
 #               0 = sweep (first time-tiled kernel; 2-D and the shapes sweep2 does not fit)
-T2_GEOM = {2: (11, 2), 1: (15, 2)}   # time_order -> (consumer warps NCW, rows per warp VY)
-
-
-def _sweep2_fits(wave: int, R: int, TK: int) -> bool:
-    if wave:
-        return TK == 2 and R <= 4
-    return (R == 1 and TK in (2, 4)) or (R == 2 and TK in (2, 4))
+def _sweep2_oy(wave: int, R: int, TK: int):
+    """Output rows of the sweep2 (one warp group per level) instance, or None if it does not fit
+    (<= 31 consumer warps of two rows; wave only two levels)."""
+    if TK == 2 and R <= 4:
+        return 16 if R < 4 else 14      # <= 20 warps (96 registers/thread) for R = 4
+    if not wave and TK == 4 and R <= 2:
+        return 8
+    return None
 
 
 def instances():
-    """(ndim, wave, R, TK, VY, NWY, kind) compiled into this build."""
+    """(ndim, wave, R, TK, VY, NWY, kind) compiled into this build.
+    For kind 2 the NWY slot holds the output rows OY of the instance."""
     out = []
     for wave in (0, 1):
-        to = 2 if wave else 1
         for R in range(1, 9):
             out.append((3, wave, R, 1, 1, NCW_T1, 1))
-            if _sweep2_fits(wave, R, 2):
-                ncw, vy = T2_GEOM[to]
-                out.append((3, wave, R, 2, vy, ncw, 2))
+            oy = _sweep2_oy(wave, R, 2)
+            if oy:
+                out.append((3, wave, R, 2, 2, oy, 2))
             else:
                 out.append((3, wave, R, 2) + _vy_nwy(3, R, 2) + (0,))
         for R in range(1, 9):
@@ -61,11 +62,8 @@ def instances():
         out.append((2, wave, 1, 2) + _vy_nwy(2, 1, 2) + (0,))
         out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4) + (0,))
     for R, TK in ((1, 4), (2, 4), (1, 8)):
-        if _sweep2_fits(0, R, TK):
-            ncw, vy = T2_GEOM[1]
-            out.append((3, 0, R, TK, vy, ncw, 2))
-        else:
-            out.append((3, 0, R, TK) + _vy_nwy(3, R, TK) + (0,))
+        oy = _sweep2_oy(0, R, TK)
+        out.append((3, 0, R, TK, 2, oy, 2) if oy else (3, 0, R, TK) + _vy_nwy(3, R, TK) + (0,))
     return out
 
 
@@ -82,7 +80,7 @@ def _gen_sources(groups: int, inst=None, outdir: str = BUILD, ncw: int = NCW_T1)
             if kind == 1:
                 lines.append(f"  make_entry1<{R}, {w}, {ndim}, {ncw}>(),")
             elif kind == 2:
-                lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}, {VY}>(),")
+                lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}>(),")   # NWY = output rows
             else:
                 lines.append(f"  make_entry<{R}, {TK}, {w}, {ndim}, {VY}, {NWY}>(),")
         lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]
@@ -173,7 +171,8 @@ def build_variant(name: str, defines=(), only=None, ncw: int = NCW_T1, verbose: 
     if only is not None:
         inst = [i for i in inst if tuple(i[:4]) in set(map(tuple, only))]
     outdir = os.path.join(HERE, "_variants", name)
-    lib = os.path.join(HERE, "_variants", f"libstencil_{name}.so")
+    os.makedirs(os.path.join(HERE, "_varlib"), exist_ok=True)
+    lib = os.path.join(HERE, "_varlib", f"libstencil_{name}.so")   # shipped to the GPU box
     return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose, ncw=ncw)
 
 

@@ -533,6 +533,7 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
     sp.out_lo = (int)(p->has_lo ? p->G - shrink : p->G);
     sp.out_hi = (int)(p->has_hi ? p->G + p->nzl + shrink : p->G + p->nzl);
     sp.P = bufs[prev];
+    sp.C = bufs[cur];
     int new_prev, new_cur;
     if (!tiled) {
       sp.outP = bufs[prev];            // in place: u^{n+1} over u^{n-1}

@@ -96,17 +96,17 @@ constexpr KernelEntry make_entry1() {
                      &launch_sweep1<R, WAVE, NDIM, NCW>, &query_sweep1<R, WAVE, NDIM, NCW>, ST_T1_DEPTH};
 }
 
-// ---- warp-specialised time-tiled kernel (sweep2.cuh)
-template <int R, int TK, bool WAVE, int NCW, int VY>
+// ---- warp-specialised time-tiled kernel (sweep2.cuh): one warp group per level
+template <int R, int TK, bool WAVE, int OY>
 cudaError_t launch_sweep2(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  sweep2_kernel<R, TK, WAVE, NCW, VY><<<grid, 32 * (NCW + 1), smem, stream>>>(map, p, nslot);
+  sweep2_kernel<R, TK, WAVE, OY><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(map, p, nslot);
   return cudaGetLastError();
 }
 
-template <int R, int TK, bool WAVE, int NCW, int VY>
+template <int R, int TK, bool WAVE, int OY>
 cudaError_t query_sweep2(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweep2_kernel<R, TK, WAVE, NCW, VY>;
+  auto k = sweep2_kernel<R, TK, WAVE, OY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (attr) {
@@ -121,13 +121,12 @@ cudaError_t query_sweep2(size_t smem, cudaFuncAttributes* attr, int* bps, int nt
 #define ST_T2_DEPTH 3   // time-tiled kernel: ring planes of prefetch beyond the radius+1 in use
 #endif
 
-template <int R, int TK, bool WAVE, int NCW, int VY>
+template <int R, int TK, bool WAVE, int OY>
 constexpr KernelEntry make_entry2() {
-  using G = Geom2<R, TK, WAVE, NCW, VY>;
-  return KernelEntry{3, WAVE ? 2 : 1, R, TK, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+  using G = Geom2<R, TK, WAVE, OY>;
+  return KernelEntry{3, WAVE ? 2 : 1, R, TK, 2, G::NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      R, (size_t)G::SLOT_BYTES, (size_t)G::FIXED_BYTES,
-                     &launch_sweep2<R, TK, WAVE, NCW, VY>, &query_sweep2<R, TK, WAVE, NCW, VY>,
-                     ST_T2_DEPTH};
+                     &launch_sweep2<R, TK, WAVE, OY>, &query_sweep2<R, TK, WAVE, OY>, ST_T2_DEPTH};
 }
 
 }  // namespace st

@@ -34,6 +34,7 @@ struct SweepParams {
   int out_lo, out_hi;         // planes this pass must produce (last level)
   int zchunk;                 // output planes per CTA (gridDim.z chunks)
   const float* P;             // u^{n-1}
+  const float* C;             // u^n (also read through the tensor map)
   float* outP;                // TK==1: u^{n+1} (may alias P); TK>1: u^{n+TK-1}
   float* outC;                // TK>1: u^{n+TK}
   const float4* ac;           // medium {a(x),a(x+1),c(x),c(x+1)} per column pair; row = X/2 float4

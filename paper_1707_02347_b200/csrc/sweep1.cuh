@@ -72,6 +72,9 @@ struct Geom1 {
 #ifndef ST_PD
 #define ST_PD 4
 #endif
+#ifndef ST_ROT1
+#define ST_ROT1 0
+#endif
   static constexpr int PD = ST_PD;                 // cp.async staging distance (planes)
   static constexpr int STAGE_F = 64 + 128;         // one staged plane row: u^{n-1} (64) + {a,c} (128)
   static constexpr int STAGE_BYTES = NCW * (PD + 1) * STAGE_F * 4;
@@ -184,10 +187,14 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
                                        // (the first centre, plane zb, is arrival RZ)
   uint32_t ph_a = 0;
 
-  for (int base = 0; base < n_arr; base += QN) {
+  // ST_ROT1: the z-queue is rotated by register moves after every step (code = one step body)
+  // instead of unrolling the loop by the queue length (code = QN step bodies).
+  constexpr int UNR = ST_ROT1 ? 1 : QN;
+  for (int base = 0; base < n_arr; base += UNR) {
 #pragma unroll
-    for (int u = 0; u < QN; ++u) {
-      const int idx = base + u;
+    for (int uu = 0; uu < UNR; ++uu) {
+      const int u = ST_ROT1 ? QN - 1 : uu;
+      const int idx = base + uu;
       if (idx < n_arr) {
         mbar_wait(&full[slot_a], ph_a);
         qn[u] = lds64(ring + slot_a * SLOT_F + col);
@@ -239,6 +246,10 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
           out += plane;
         }
         if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
+        if (ST_ROT1) {
+#pragma unroll
+          for (int i = 0; i + 1 < QN; ++i) qn[i] = qn[i + 1];
+        }
       }
     }
   }

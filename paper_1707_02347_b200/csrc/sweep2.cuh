@@ -1,103 +1,379 @@
-// sweep2.cuh -- time-tiled (TK levels per pass) 3-D sweep for sm_100a, warp-specialised.
+// sweep2.cuh -- time-tiled (TK levels per pass) 3-D sweep for sm_100a: one warp group per level.
 //
 // The paper's method (time tiling; the CLooG schedule P:1437-1501) re-derived for
 // a GPU (DESIGN.md §6 G2):
-//   * one CTA owns a 64-column x GH-row x-y region and streams z;
-//   * level l of the pass computes plane s - l*r while the TMA front is at plane s + r -- the
-//     paper's skew of the time-tiled band by the stencil radius (P:1196-1202, P:1445
-//     "int skew = 4*time"), applied to the streamed axis as a wavefront lag;
-//   * the x-y region of level l shrinks by r per level (overlapped tiles: the redundant halo
-//     work replaces the paper's sequential skewed tile order, which would serialise the SMs);
-//   * only the last two levels (u^{n+TK-1}, u^{n+TK}) are written to HBM.
-// Roles:
+//   * one CTA owns a 64-column x GH-row x-y region (GH = OY + 2r(TK-1)) and streams z;
+//   * at step a, level l computes plane p_first + a - (l+1)r: each level trails the one below it
+//     by r planes -- the paper's skew of the time-tiled band by the stencil radius (P:1196-1202,
+//     P:1445 "int skew = 4*time"), applied to the streamed axis as a wavefront lag;
+//   * the x-y region shrinks by r per level (overlapped tiles: the redundant halo work replaces
+//     the paper's sequential skewed tile order, which would serialise the SMs);
+//   * only the last two levels (u^{n+TK-1}, u^{n+TK}) of the output tile are written to HBM.
+// Roles (a software pipeline across warp groups, no __syncthreads in the steady state):
 //   * warp NCW (producer): one lane TMA-loads every u^n plane box (region + r halo, out-of-bounds
 //     zero fill = Dirichlet boundary) into a ring of mbarrier-tracked slots (full/empty);
-//   * warps 0..NCW-1 (consumers): warp w owns rows [w*VY, (w+1)*VY) of the region at every level,
-//     a column PAIR per lane (packed fp32x2).  Each level's z-column is a register queue of 2r+1
-//     planes; the in-plane neighbours of level l >= 1 come from a shared-memory ring of level
-//     l-1 planes with its own full/empty mbarriers (every consumer lane arrives).  No
-//     __syncthreads in the steady state: warps drift within the ring depths.
-//   * u^{n-1} and the medium of every level's plane are staged PD steps ahead with cp.async.
-// Arithmetic is the canonical per-point order of include/stencil.h, so every value is
-// bit-identical to the untiled sweep and to the CPU oracle (oracle/, never included here).
+//   * group l (warps(l) warps, two rows each, a column PAIR per lane, packed fp32x2) computes
+//     level l.  Its input planes come from the TMA ring (l = 0) or from the shared-memory ring of
+//     level l-1 (each slot guarded by a full/empty mbarrier pair); it keeps the z-column of its
+//     rows in a register queue of 2r+1 planes and takes the x/y neighbours from the centre plane
+//     in shared memory.  Levels below TK-1 publish every plane into their own ring; the last
+//     level writes u^{n+TK}, u^{n+TK-1} to global memory.
+//   * u^{n-1} (level 0), u^n (level 1) and the medium of each level's plane are staged PD steps
+//     ahead with cp.async (wave; the medium a, c is read once per level, from L2 after level 0).
+// All shared-memory traffic uses 32-bit shared-window addresses.  Arithmetic is the canonical
+// per-point order of include/stencil.h, so every value is bit-identical to the untiled sweep and
+// to the CPU oracle (oracle/, never included here).
 #pragma once
 #include "sweep1.cuh"
 
 namespace st {
 
-template <int R, int TK, bool WAVE, int NCW, int VY>
+// ------------------------------------------------------------ 32-bit shared-window primitives
+template <int OFF>
+__device__ __forceinline__ uint64_t ld_s64(uint32_t a) {
+  uint64_t v; asm volatile("ld.shared.b64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(OFF)); return v;
+}
+__device__ __forceinline__ uint64_t ld_s64r(uint32_t a) {
+  uint64_t v; asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a)); return v;
+}
+__device__ __forceinline__ float4 ld_s128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void st_s64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.b64 [%0], %1;" :: "r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mb_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(a) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred q;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 0x989680;\n\t"
+                 "selp.u32 %0, 1, 0, q;\n\t}"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_3d_s(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                              int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+
+template <int R, int TK, bool WAVE, int OY_>
 struct Geom2 {
-  static constexpr int RZ = R;                     // 3-D only
-  static constexpr int QN = 2 * R + 1;
-  static constexpr int RX2 = (R + 1) & ~1;
-  static constexpr int RXB = (R + 3) & ~3;
+  static constexpr int VY = 2;                     // rows per warp
   static constexpr int GW = 64;
-  static constexpr int GH = NCW * VY;
-  static constexpr int HX0 = Halo<R, TK>::hx(0);
-  static constexpr int HY0 = R * (TK - 1);
+  static constexpr int QN = 2 * R + 1;
+  static constexpr int OY = OY_;
+  static constexpr int GH = OY + 2 * (TK - 1) * R; // level-0 rows
+  static constexpr int rows(int l) { return GH - 2 * l * R; }
+  static constexpr int warps(int l) { return rows(l) / VY; }
+  static constexpr int wbase(int l) { return l == 0 ? 0 : wbase(l - 1) + warps(l - 1); }
+  static constexpr int NCW = wbase(TK);            // consumer warps over all levels
+  static constexpr int NTHREADS = 32 * (NCW + 1);
+  static constexpr int RXB = (R + 3) & ~3;
+  static constexpr int HX0 = Halo<R, TK>::hx(0);   // level-0 x halo (even)
   static constexpr int XS = HX0 % 4;               // keep the TMA box start 16-B aligned
   static constexpr int BW = GW + 2 * RXB + (XS ? 8 : 0);
   static constexpr int BH = GH + 2 * R;
   static constexpr int BCOL = RXB + XS;
   static constexpr int OX = GW - 2 * HX0;
-  static constexpr int OY = GH - 2 * HY0;
   static constexpr int SLOT_BYTES = ((BW * BH * 4) + 127) / 128 * 128;
-  static constexpr int DL = R + 3;                 // level-ring depth (planes); >= R + 1 needed
-  static constexpr int LVL_F = GW * (GH + 2 * R);  // one level plane + R pad rows above/below
-  static constexpr int LVL_BYTES = LVL_F * 4;
+#ifndef ST_DL2
+#define ST_DL2 3
+#endif
+  static constexpr int DL = R + ST_DL2;            // level-ring depth (planes); >= R + 1 needed
+  static constexpr int LVL_BYTES = GW * (GH + 2 * R) * 4;   // one plane + R pad rows each side
 #ifndef ST_PD2
 #define ST_PD2 2
 #endif
   static constexpr int PD = ST_PD2;                // cp.async staging distance (steps)
-  static constexpr int STAGE_F = WAVE ? VY * (64 + 128 * TK) : 0;   // prev + medium per level
-  static constexpr int BAR_BYTES = 2048;
-  static constexpr int FIXED_BYTES =
-      BAR_BYTES + (TK - 1) * DL * LVL_BYTES + NCW * (PD + 1) * STAGE_F * 4;
-  static constexpr int NTHREADS = 32 * (NCW + 1);
-  static_assert(TK >= 2, "sweep2 is the time-tiled kernel");
-  static_assert(OX > 0 && OY > 0, "tile too small for this radius / depth");
+  // staging entry (wave): [2 rows x 64: u^{n-1} (level 0) or u^n (level 1)][2 rows x 128: a, c]
+  static constexpr int STAGE_BYTES = WAVE ? (2 * 64 + 2 * 128) * 4 : 0;
+  static constexpr int BAR_BYTES = 2048;           // full[64] | empty[64] | lfull[TK-1][DL] | lempty[TK-1][DL]
+  static constexpr int LRING_OFF = BAR_BYTES;
+  static constexpr int STAGE_OFF = LRING_OFF + (TK - 1) * DL * LVL_BYTES;
+  static constexpr int FIXED_BYTES = STAGE_OFF + NCW * (PD + 1) * STAGE_BYTES;
+  static_assert(TK >= 2 && (!WAVE || TK == 2), "time-tiled kernel: wave TK = 2, heat TK >= 2");
+  static_assert(OY % 2 == 0 && NCW + 1 <= 32, "warp budget");
+  static_assert(OX > 0, "tile too small for this radius / depth");
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
-  static_assert(8 * (2 * 64 + 2 * (TK - 1) * DL) <= BAR_BYTES, "barrier area");
+  static_assert(8 * (128 + 2 * (TK - 1) * DL) <= BAR_BYTES, "barrier area");
+  static_assert(FIXED_BYTES % 128 == 0, "TMA ring alignment");
 };
 
-template <int R, int TK, bool WAVE, int NCW, int VY>
-__global__ void __launch_bounds__(32 * (NCW + 1), 1)
+// x/y/z accumulation of two rows (canonical order, include/stencil.h).  cb: shared address of
+// (my first row, my pair) in the centre plane; PB: plane row pitch in bytes; q: z-queue whose
+// centre is q[R].
+template <int R, int PB>
+__device__ __forceinline__ void accum2(uint64_t (&acc)[2], const uint64_t (&q)[2 * R + 1][2],
+                                       uint32_t cb, const SweepParams& p) {
+  constexpr int RX2 = (R + 1) & ~1;
+  const uint64_t K0 = splat(p.K0);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint32_t rb = cb + j * PB;
+    const uint64_t c = q[R][j];
+    uint64_t A[RX2 + 1];
+#pragma unroll
+    for (int m = -RX2 / 2; m <= RX2 / 2; ++m) {
+      A[m + RX2 / 2] = (m == 0) ? c : ld_s64r(rb + 8 * m);
+    }
+    uint64_t a = f2mul(K0, c);
+#pragma unroll
+    for (int k = 1; k <= R; ++k) {
+      uint64_t sx;
+      if ((k & 1) == 0) {
+        sx = f2add(A[RX2 / 2 - k / 2], A[RX2 / 2 + k / 2]);
+      } else {   // odd offset: element sums taken from neighbouring aligned pairs
+        const uint64_t Lm = A[RX2 / 2 - (k + 1) / 2], L0 = A[RX2 / 2 - (k - 1) / 2];
+        const uint64_t R0 = A[RX2 / 2 + (k - 1) / 2], Rp = A[RX2 / 2 + (k + 1) / 2];
+        sx = pack2(fadd_ftz(hi_of(Lm), hi_of(R0)), fadd_ftz(lo_of(L0), lo_of(Rp)));
+      }
+      a = f2fma(splat(p.W[0][k]), sx, a);
+      const uint64_t yl = (j - k >= 0) ? q[R][(j - k) >= 0 ? (j - k) : 0] : ld_s64r(rb - k * PB);
+      const uint64_t yr = (j + k < 2) ? q[R][(j + k) < 2 ? (j + k) : 0] : ld_s64r(rb + k * PB);
+      a = f2fma(splat(p.W[1][k]), f2add(yl, yr), a);
+      a = f2fma(splat(p.W[2][k]), f2add(q[R - k][j], q[R + k][j]), a);
+    }
+    acc[j] = a;
+  }
+}
+
+// One consumer warp of level L (group L): the whole z stream of the CTA's chunk.
+template <int L, int R, int TK, bool WAVE, int OY>
+__device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot, const uint32_t sbase,
+                                           const int warp, const int lane, const int tx0,
+                                           const int ty0, const int zb, const int ze) {
+  using G = Geom2<R, TK, WAVE, OY>;
+  constexpr int QN = G::QN, GW = G::GW, BW = G::BW, DL = G::DL, PD = G::PD, GH = G::GH;
+  constexpr int HX0 = G::HX0, HY0 = (TK - 1) * R;
+  constexpr int SLOT = G::SLOT_BYTES, LVL = G::LVL_BYTES, STB = G::STAGE_BYTES;
+  constexpr int PB = (L == 0) ? BW * 4 : GW * 4;   // input-plane row pitch (bytes)
+  const int wl = warp - G::wbase(L);
+  const int r0 = L * R + 2 * wl;                    // region row of my first row
+  const int gx = tx0 - HX0, gy = ty0 - HY0;
+  const int x0 = gx + 2 * lane;
+  const bool xin0 = (x0 >= 0) && (x0 < p.nx);
+  const bool xin1 = (x0 + 1 >= 0) && (x0 + 1 < p.nx);
+  const uint64_t xmask = (xin0 ? 0xffffffffull : 0ull) | (xin1 ? 0xffffffff00000000ull : 0ull);
+  const int y0 = gy + r0;
+  const bool yin0 = (y0 >= 0) && (y0 < p.ny), yin1 = (y0 + 1 >= 0) && (y0 + 1 < p.ny);
+  const uint64_t m0 = yin0 ? xmask : 0ull, m1 = yin1 ? xmask : 0ull;
+  const bool lane_out = (lane >= HX0 / 2) && (lane < 32 - HX0 / 2);   // output-tile lanes
+  const bool row0_out = r0 >= HY0 && r0 < GH - HY0, row1_out = r0 + 1 >= HY0 && r0 + 1 < GH - HY0;
+  const int p_first = zb - TK * R;
+  const int n_arr = (ze - zb) + 2 * TK * R;
+  // level L at step a computes plane p_first + a - (L+1)R; active on [a_lo, a_hi)
+  const int q_lo = max(zb - (TK - 1 - L) * R, p.gz_lo), q_hi = min(ze + (TK - 1 - L) * R, p.gz_hi);
+  const int a_lo = q_lo - p_first + (L + 1) * R, a_hi = q_hi - p_first + (L + 1) * R;
+
+  // rare events (warp-uniform)
+  bool wsrc = false, wrec = false;
+  if (q_lo < q_hi) {
+    if (yin0) wsrc |= row_has_entry(p.src_begin, p.src, q_lo, q_hi, y0, gx, gx + 64);
+    if (yin1) wsrc |= row_has_entry(p.src_begin, p.src, q_lo, q_hi, y0 + 1, gx, gx + 64);
+  }
+  if (yin0 && row0_out) wrec |= row_has_entry(p.rec_begin, p.rec, zb, ze, y0, tx0, tx0 + G::OX);
+  if (yin1 && row1_out) wrec |= row_has_entry(p.rec_begin, p.rec, zb, ze, y0 + 1, tx0, tx0 + G::OX);
+  wsrc = __any_sync(0xffffffffu, wsrc);
+  wrec = __any_sync(0xffffffffu, wrec);
+
+  // shared-window addresses
+  const uint32_t b_full = sbase, b_empty = sbase + 512;
+  const uint32_t b_lf = sbase + 1024, b_le = sbase + 1024 + 8 * (TK - 1) * DL;
+  const uint32_t lf_in = b_lf + 8 * ((L > 0 ? L - 1 : 0) * DL), le_in = b_le + 8 * ((L > 0 ? L - 1 : 0) * DL);
+  const uint32_t lf_out = b_lf + 8 * ((L < TK - 1 ? L : 0) * DL), le_out = b_le + 8 * ((L < TK - 1 ? L : 0) * DL);
+  const uint32_t ring_in = (L == 0) ? sbase + G::FIXED_BYTES
+                                    : sbase + G::LRING_OFF + (L > 0 ? L - 1 : 0) * DL * LVL;
+  const uint32_t ring_out = sbase + G::LRING_OFF + (L < TK - 1 ? L : 0) * DL * LVL;
+  const uint32_t my_in = (L == 0) ? ((r0 + R) * BW + G::BCOL + 2 * lane) * 4 : ((r0 + R) * GW + 2 * lane) * 4;
+  const uint32_t my_out = ((r0 + R) * GW + 2 * lane) * 4;
+  const uint32_t stage = sbase + G::STAGE_OFF + warp * (PD + 1) * STB;
+
+  // ---- staging (wave): level 0: u^{n-1}, a/c of its plane; level 1: u^n, a/c of its plane ----
+  const long long plane = p.plane;
+  const float* gsrc = (L == 0) ? p.P : p.C;
+  long long soff = (long long)(p_first - (L + 1) * R) * plane + (long long)y0 * p.X + x0;
+  const int X = p.X;
+  int a_iss = 0, e_iss = 0, e_use = 0;
+  auto stage_next = [&]() {
+    if (xin0 && a_iss >= a_lo && a_iss < a_hi) {
+      const uint32_t e = stage + e_iss * STB;
+      const float* g = gsrc + soff;
+      const float4* ga = p.ac + (soff >> 1);
+      if (yin0) { cp_async8_s(e + 8 * lane, g); cp_async16_s(e + 512 + 16 * lane, ga); }
+      if (yin1) { cp_async8_s(e + 256 + 8 * lane, g + X); cp_async16_s(e + 1024 + 16 * lane, ga + (X >> 1)); }
+    }
+    cp_async_commit();
+    ++a_iss;
+    soff += plane;
+    if (++e_iss == PD + 1) e_iss = 0;
+  };
+  if (WAVE) {
+#pragma unroll 1
+    for (int i = 0; i < PD; ++i) stage_next();
+  }
+
+  uint64_t q[QN][2];
+#pragma unroll
+  for (int i = 0; i < QN; ++i) q[i][0] = q[i][1] = 0ull;
+
+  // ring counters
+  int in_slot = 0;  uint32_t in_ph = 0;            // input slot of step a
+  int c_slot = (L == 0) ? (R % nslot) : 0;         // centre slot (TMA: arrival a-R; ring: step a-R)
+  int out_slot = 0; uint32_t out_ph = 0;           // output ring slot of step a
+  const uint64_t DT = splat(p.dt);
+  const bool wr_prev = WAVE || p.write_prev;
+  const long long obase = (long long)(p_first - TK * R) * plane + (long long)y0 * X + x0;
+
+#pragma unroll 1
+  for (int a = 0; a < n_arr; ++a) {
+    // ---- input plane of step a into the queue ----------------------------------------------
+    if (L == 0) {
+      mb_wait(b_full + 8 * in_slot, in_ph);
+      const uint32_t s = ring_in + in_slot * SLOT + my_in;
+      q[QN - 1][0] = ld_s64<0>(s);
+      q[QN - 1][1] = ld_s64<PB>(s);
+      if (a < R) mb_arrive(b_empty + 8 * in_slot);   // never a centre plane
+      if (++in_slot == nslot) { in_slot = 0; in_ph ^= 1u; }
+    } else {
+      mb_wait(lf_in + 8 * in_slot, in_ph);
+      const uint32_t s = ring_in + in_slot * LVL + my_in;
+      q[QN - 1][0] = ld_s64<0>(s);
+      q[QN - 1][1] = ld_s64<PB>(s);
+      if (++in_slot == DL) { in_slot = 0; in_ph ^= 1u; }
+    }
+    if (WAVE) stage_next();
+
+    // ---- level L at plane p_first + a - (L+1)R ----------------------------------------------
+    uint64_t o0 = 0ull, o1 = 0ull;
+    const bool centre = (L == 0) ? (a >= 2 * R) : (a >= R);
+    if (centre) {
+      if (a >= a_lo && a < a_hi) {
+        if (WAVE) cp_async_wait<PD>();              // this step's staged group has landed
+        const int qp = p_first + a - (L + 1) * R;
+        const uint32_t cb = ring_in + c_slot * ((L == 0) ? SLOT : LVL) + my_in;
+        uint64_t acc[2];
+        accum2<R, PB>(acc, q, cb, p);
+        if (wsrc) {
+          if (yin0) acc[0] = add_sources_row(acc[0], p, qp, y0, x0, p.wl_step + L);
+          if (yin1) acc[1] = add_sources_row(acc[1], p, qp, y0 + 1, x0, p.wl_step + L);
+        }
+        const uint64_t c0 = q[R][0], c1 = q[R][1];
+        if (WAVE) {
+          const uint32_t e = stage + e_use * STB;
+          const uint64_t p0 = ld_s64r(e + 8 * lane), p1 = ld_s64r(e + 256 + 8 * lane);
+          const float4 a0 = ld_s128(e + 512 + 16 * lane), a1 = ld_s128(e + 1024 + 16 * lane);
+          o0 = f2fma(pack2(a0.z, a0.w), acc[0], f2fma(pack2(a0.x, a0.y), f2sub(p0, c0), c0));
+          o1 = f2fma(pack2(a1.z, a1.w), acc[1], f2fma(pack2(a1.x, a1.y), f2sub(p1, c1), c1));
+        } else {
+          o0 = f2fma(DT, acc[0], c0);
+          o1 = f2fma(DT, acc[1], c1);
+        }
+        o0 &= m0; o1 &= m1;
+        if (L == TK - 1) {
+          // u^{n+TK} and u^{n+TK-1} on the output tile (every row of the last group is an
+          // output row; the active range is exactly the output planes)
+          if (lane_out && xin0) {
+            const long long off = obase + (long long)a * plane;
+            float* oc = p.outC + off;
+            float* op = p.outP + off;
+            if (xin1) {
+              if (yin0) { sts64(oc, o0); if (wr_prev) sts64(op, c0); }
+              if (yin1) { sts64(oc + X, o1); if (wr_prev) sts64(op + X, c1); }
+            } else {
+              if (yin0) { oc[0] = lo_of(o0); if (wr_prev) op[0] = lo_of(c0); }
+              if (yin1) { oc[X] = lo_of(o1); if (wr_prev) op[X] = lo_of(c1); }
+            }
+          }
+        }
+        if (wrec && qp >= zb && qp < ze && lane_out) {
+          if (yin0 && row0_out) sample_receivers_row(o0, p, qp, y0, x0, p.tr_step + L);
+          if (yin1 && row1_out) sample_receivers_row(o1, p, qp, y0 + 1, x0, p.tr_step + L);
+        }
+      }
+      // release the centre plane
+      if (L == 0) {
+        mb_arrive(b_empty + 8 * c_slot);
+        if (++c_slot == nslot) c_slot = 0;
+      } else {
+        mb_arrive(le_in + 8 * c_slot);
+        if (++c_slot == DL) c_slot = 0;
+      }
+    }
+    if (WAVE && ++e_use == PD + 1) e_use = 0;
+
+    // ---- publish level L's plane into its ring (levels below the last) -----------------------
+    if (L < TK - 1) {
+      if (a >= DL) mb_wait(le_out + 8 * out_slot, out_ph ^ 1u);
+      const uint32_t d = ring_out + out_slot * LVL + my_out;
+      st_s64(d, o0);
+      st_s64(d + GW * 4, o1);
+      mb_arrive(lf_out + 8 * out_slot);
+      if (++out_slot == DL) { out_slot = 0; out_ph ^= 1u; }
+    }
+
+    // ---- rotate the z-queue -------------------------------------------------------------------
+#pragma unroll
+    for (int i = 0; i + 1 < QN; ++i) { q[i][0] = q[i + 1][0]; q[i][1] = q[i + 1][1]; }
+  }
+  if (WAVE) cp_async_wait<0>();
+}
+
+template <int L, int R, int TK, bool WAVE, int OY>
+__device__ __forceinline__ void dispatch_level(int l, const SweepParams& p, int nslot, uint32_t sbase,
+                                               int warp, int lane, int tx0, int ty0, int zb, int ze) {
+  if (l == L) {
+    level_warp<L, R, TK, WAVE, OY>(p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
+  } else if constexpr (L + 1 < TK) {
+    dispatch_level<L + 1, R, TK, WAVE, OY>(l, p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
+  }
+}
+
+template <int R, int TK, bool WAVE, int OY>
+__global__ void __launch_bounds__(Geom2<R, TK, WAVE, OY>::NTHREADS, 1)
 sweep2_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
               const int nslot) {
-  using G = Geom2<R, TK, WAVE, NCW, VY>;
-  constexpr int QN = G::QN, RX2 = G::RX2, BW = G::BW, GW = G::GW, GH = G::GH, DL = G::DL;
-  constexpr int HX0 = G::HX0, HY0 = G::HY0, BCOL = G::BCOL;
-  constexpr int SLOT_F = G::SLOT_BYTES / 4, PD = G::PD, STAGE_F = G::STAGE_F;
-  constexpr int NL = TK - 1;                        // levels with a shared-memory ring
-
+  using G = Geom2<R, TK, WAVE, OY>;
+  constexpr int NCW = G::NCW, DL = G::DL;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + 64;
-  uint64_t* lfull = empty + 64;                     // [NL][DL]
-  uint64_t* lempty = lfull + NL * DL;               // [NL][DL]
-  float* lring = reinterpret_cast<float*>(smem + G::BAR_BYTES);
-  float* stage_all = lring + (size_t)NL * DL * G::LVL_F;
-  float* ring = stage_all + (size_t)NCW * (PD + 1) * STAGE_F;   // 128-B aligned (sizes are)
-
+  const uint32_t sbase = smem_u32(smem);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int tx0 = blockIdx.x * G::OX, ty0 = blockIdx.y * G::OY;   // output tile origin
-  const int gx = tx0 - HX0, gy = ty0 - HY0;                      // region origin
   const int zb = p.out_lo + blockIdx.z * p.zchunk;
   const int ze = min(p.out_hi, zb + p.zchunk);
   if (zb >= ze) return;
-  const int p_first = zb - TK * R;                  // first u^n plane (arrival 0)
-  const int n_arr = (ze - zb) + 2 * TK * R;
 
   if (tid == 0) {
     for (int i = 0; i < nslot; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 32 * NCW);
+      mb_init(sbase + 8 * i, 1);                          // full: producer's expect_tx
+      mb_init(sbase + 512 + 8 * i, 32 * G::warps(0));     // empty: level-0 lanes
     }
-    for (int i = 0; i < NL * DL; ++i) {
-      mbar_init(&lfull[i], 32 * NCW);
-      mbar_init(&lempty[i], 32 * NCW);
-    }
+    for (int l = 0; l + 1 < TK; ++l)
+      for (int i = 0; i < DL; ++i) {
+        mb_init(sbase + 1024 + 8 * (l * DL + i), 32 * G::warps(l));                         // writers
+        mb_init(sbase + 1024 + 8 * ((TK - 1) * DL + l * DL + i), 32 * G::warps(l + 1));     // readers
+      }
     fence_mbar_init();
   }
   __syncthreads();
@@ -106,276 +382,25 @@ sweep2_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     // ------------------------------------------------------------------ producer warp
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmapC)) : "memory");
+      const int p_first = zb - TK * R, n_arr = (ze - zb) + 2 * TK * R;
+      const int gx = tx0 - G::HX0, gy = ty0 - (TK - 1) * R;
+      const uint32_t ring = sbase + G::FIXED_BYTES;
       int slot = 0;
       uint32_t ph = 0;
       for (int a = 0; a < n_arr; ++a) {
-        if (a >= nslot) mbar_wait(&empty[slot], ph ^ 1u);
-        mbar_expect_tx(&full[slot], (uint32_t)(BW * G::BH * 4));
-        tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &full[slot], gx - BCOL, gy - R,
-                    p_first + a - p.zv_lo);
+        if (a >= nslot) mb_wait(sbase + 512 + 8 * slot, ph ^ 1u);
+        mb_expect_tx(sbase + 8 * slot, (uint32_t)(G::BW * G::BH * 4));
+        tma_load_3d_s(ring + slot * G::SLOT_BYTES, &tmapC, sbase + 8 * slot, gx - G::BCOL, gy - R,
+                      p_first + a - p.zv_lo);
         if (++slot == nslot) { slot = 0; ph ^= 1u; }
       }
     }
     return;
   }
-
-  // -------------------------------------------------------------------- consumer warps
-  const int x0 = gx + 2 * lane;                     // my column pair
-  const int ry = warp * VY;                         // my first region row
-  const int y0 = gy + ry;                           // my first interior row
-  const bool xin0 = (x0 >= 0) && (x0 < p.nx);
-  const bool xin1 = (x0 + 1 >= 0) && (x0 + 1 < p.nx);
-  const uint64_t xmask = (xin0 ? 0xffffffffull : 0ull) | (xin1 ? 0xffffffff00000000ull : 0ull);
-  uint64_t rmask[VY];
-  bool yin[VY];
+  int l = 0;
 #pragma unroll
-  for (int j = 0; j < VY; ++j) {
-    yin[j] = (y0 + j >= 0) && (y0 + j < p.ny);
-    rmask[j] = yin[j] ? xmask : 0ull;
-  }
-  bool any_row = false;
-#pragma unroll
-  for (int j = 0; j < VY; ++j) any_row |= yin[j];
-  const bool act = any_row && xin0;                 // this lane owns >= 1 interior point
-  const uint64_t K0 = splat(p.K0);
-  const uint64_t DT = splat(p.dt);
-  // level l is computed on lanes [ex_l, 32-ex_l) and region rows [l*R, GH-l*R)
-  // the last level's rows/lanes are the output tile
-  const int ex_last = (HX0 - Halo<R, TK>::hx(TK - 1)) / 2;
-  const bool lane_out = (lane >= ex_last) && (lane < 32 - ex_last);
-
-  // rare events: does any of my rows hold a source (any level plane) / receiver (output planes)?
-  bool wsrc = false, wrec = false;
-#pragma unroll
-  for (int j = 0; j < VY; ++j) {
-    if (yin[j]) {
-      const int zl = max(zb - (TK - 1) * R, p.gz_lo), zh = min(ze + (TK - 1) * R, p.gz_hi);
-      if (zl < zh) wsrc |= row_has_entry(p.src_begin, p.src, zl, zh, y0 + j, gx, gx + 64);
-      wrec |= row_has_entry(p.rec_begin, p.rec, zb, ze, y0 + j, tx0, tx0 + G::OX);
-    }
-  }
-  wsrc = __any_sync(0xffffffffu, wsrc);
-  wrec = __any_sync(0xffffffffu, wrec);
-
-  // level l at arrival a computes plane a + p_first - (l+1)R, inside its range and the domain
-  auto level_on = [&](int l, int a) -> bool {
-    const int q = p_first + a - (l + 1) * R;
-    return (q >= zb - (TK - 1 - l) * R) && (q < ze + (TK - 1 - l) * R) && (q >= p.gz_lo) &&
-           (q < p.gz_hi);
-  };
-
-  // ---- staging of u^{n-1}(s) and the medium of every level's plane, PD steps ahead ----------
-  const long long plane = p.plane;
-  float* stage = stage_all + (size_t)warp * (PD + 1) * STAGE_F;
-  const int rowoff = y0 * p.X + x0;                 // element offset of (first row, pair)
-  const int X2 = p.X >> 1;
-  const int acoff = y0 * X2 + (x0 >> 1);
-  int a_iss = 0;                                    // next step to stage
-  int e_iss = 0, e_use = 0;
-  auto stage_next = [&]() {
-    if (a_iss < n_arr && act) {
-      float* e = stage + e_iss * STAGE_F;
-      if (level_on(0, a_iss)) {
-        const long long s = p_first + a_iss - R;
-        const float* gP = p.P + s * plane + rowoff;
-#pragma unroll
-        for (int j = 0; j < VY; ++j)
-          if (yin[j]) cp_async8(e + j * 64 + 2 * lane, gP + j * p.X);
-      }
-#pragma unroll
-      for (int l = 0; l < TK; ++l) {
-        if (level_on(l, a_iss)) {
-          const long long q = p_first + a_iss - (l + 1) * R;
-          const float4* gA = p.ac + q * (plane >> 1) + acoff;
-#pragma unroll
-          for (int j = 0; j < VY; ++j)
-            if (yin[j]) cp_async16(e + VY * 64 + (l * VY + j) * 128 + 4 * lane, gA + j * X2);
-        }
-      }
-    }
-    cp_async_commit();
-    ++a_iss;
-    if (++e_iss == PD + 1) e_iss = 0;
-  };
-  if (WAVE) {
-#pragma unroll 1
-    for (int i = 0; i < PD; ++i) stage_next();
-  }
-
-  uint64_t qn[QN][VY];                              // u^n column queue (arrival-indexed)
-  uint64_t ql[NL][QN][VY];                          // level l output queue, l = 0..TK-2
-#pragma unroll
-  for (int i = 0; i < QN; ++i)
-#pragma unroll
-    for (int j = 0; j < VY; ++j) {
-      qn[i][j] = 0ull;
-#pragma unroll
-      for (int l = 0; l < NL; ++l) ql[l][i][j] = 0ull;
-    }
-
-  int slot_a = 0;                                   // TMA ring slot of arrival a
-  uint32_t ph_a = 0;
-  int slot_c = R % nslot;                           // TMA ring slot of arrival a - R (centre);
-                                                    // the first centre is arrival R (step 2R)
-  int lslot_w = 0;                                  // level-ring slot written at step a
-  uint32_t lph_w = 0;                               // parity of its previous use (empty wait)
-  int lslot_r = 0;                                  // level-ring slot read at step a (plane a-R)
-  uint32_t lph_r = 0;
-  const int col = (ry + R) * BW + 2 * lane + BCOL;  // my first row, my pair, in a TMA slot
-  const int lcol = (ry + R) * GW + 2 * lane;        // same in a level plane
-
-  for (int base = 0; base < n_arr; base += QN) {
-#pragma unroll
-    for (int u = 0; u < QN; ++u) {
-      const int a = base + u;
-      if (a < n_arr) {
-        // ---- arrival a: u^n plane p_first + a into the queue ----------------------------
-        mbar_wait(&full[slot_a], ph_a);
-        const float* sa = ring + slot_a * SLOT_F + col;
-#pragma unroll
-        for (int j = 0; j < VY; ++j) qn[u][j] = lds64(sa + j * BW);
-        if (a < R) mbar_arrive(&empty[slot_a]);    // never a centre plane
-        if (WAVE) stage_next();
-        const float* st_e = stage + e_use * STAGE_F;
-        if (WAVE && a >= 2 * R) cp_async_wait<PD>();   // this step's group has landed
-
-        // ---- level 0 at plane s = p_first + a - R ---------------------------------------
-        uint64_t out[VY];
-#pragma unroll
-        for (int j = 0; j < VY; ++j) out[j] = 0ull;
-        if (a >= 2 * R) {                           // centre = arrival a - R >= R
-          const int s = p_first + a - R;
-          if (level_on(0, a)) {
-            const float* rp0 = ring + slot_c * SLOT_F + col;
-            uint64_t acc[VY];
-            accumulate<R, R, QN, VY, 3, BW>(acc, qn, rp0, p, md<QN>(u - R));
-            if (wsrc) {
-#pragma unroll
-              for (int j = 0; j < VY; ++j)
-                if (yin[j]) acc[j] = add_sources_row(acc[j], p, s, y0 + j, x0, p.wl_step);
-            }
-#pragma unroll
-            for (int j = 0; j < VY; ++j) {
-              const uint64_t c = qn[md<QN>(u - R)][j];
-              uint64_t o;
-              if (WAVE) {
-                const uint64_t pv = lds64(st_e + j * 64 + 2 * lane);
-                const float4 m4 = *reinterpret_cast<const float4*>(st_e + VY * 64 + j * 128 + 4 * lane);
-                o = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c));
-              } else {
-                o = f2fma(DT, acc[j], c);
-              }
-              out[j] = o & rmask[j];
-            }
-            if (wrec && s >= zb && s < ze && lane_out) {
-#pragma unroll
-              for (int j = 0; j < VY; ++j)
-                if (yin[j] && ry + j >= HY0 && ry + j < GH - HY0)
-                  sample_receivers_row(out[j], p, s, y0 + j, x0, p.tr_step);
-            }
-          }
-          mbar_arrive(&empty[slot_c]);              // centre slot done (x/y neighbours read)
-          if (++slot_c == nslot) slot_c = 0;
-        }
-#pragma unroll
-        for (int j = 0; j < VY; ++j) ql[0][u][j] = out[j];
-
-        // ---- levels 1..TK-1 ---------------------------------------------------------------
-        // publish level 0 (plane s) into level-ring 0 slot lslot_w, then level l >= 1 reads the
-        // ring of level l-1 at slot lslot_r (plane computed R steps ago).
-#pragma unroll
-        for (int l = 1; l < TK; ++l) {
-          uint64_t* lf = lfull + (l - 1) * DL;
-          uint64_t* le = lempty + (l - 1) * DL;
-          float* lr = lring + (size_t)(l - 1) * DL * G::LVL_F;
-          // publish level l-1 output of this step
-          if (a >= DL) mbar_wait(&le[lslot_w], lph_w ^ 1u);
-          {
-            float* dst = lr + (size_t)lslot_w * G::LVL_F + lcol;
-#pragma unroll
-            for (int j = 0; j < VY; ++j) sts64(dst + j * GW, ql[l - 1][u][j]);
-          }
-          mbar_arrive(&lf[lslot_w]);
-          // level l at plane q = p_first + a - (l+1)R: neighbours from the level-(l-1) plane
-          // published R steps ago
-          uint64_t ol[VY];
-#pragma unroll
-          for (int j = 0; j < VY; ++j) ol[j] = 0ull;
-          if (a >= R) {
-            mbar_wait(&lf[lslot_r], lph_r);
-            const int q = p_first + a - (l + 1) * R;
-            const int exl = (HX0 - Halo<R, TK>::hx(l)) / 2;
-            const int eyl = l * R;
-            const bool lane_in = (lane >= exl) && (lane < 32 - exl);
-            const bool rows_in = (ry + VY > eyl) && (ry < GH - eyl);     // warp-uniform
-            if (level_on(l, a) && rows_in) {
-              const float* rp = lr + (size_t)lslot_r * G::LVL_F + lcol;
-              uint64_t acc[VY];
-              accumulate<R, R, QN, VY, 3, GW>(acc, ql[l - 1], rp, p, md<QN>(u - R));
-              if (wsrc) {
-#pragma unroll
-                for (int j = 0; j < VY; ++j)
-                  if (yin[j]) acc[j] = add_sources_row(acc[j], p, q, y0 + j, x0, p.wl_step + l);
-              }
-#pragma unroll
-              for (int j = 0; j < VY; ++j) {
-                const uint64_t c = ql[l - 1][md<QN>(u - R)][j];
-                uint64_t o;
-                if (WAVE) {
-                  const uint64_t pv = (l == 1) ? qn[md<QN>(u - 2 * R)][j]
-                                               : ql[l >= 2 ? l - 2 : 0][md<QN>(u - 2 * R)][j];
-                  const float4 m4 =
-                      *reinterpret_cast<const float4*>(st_e + VY * 64 + (l * VY + j) * 128 + 4 * lane);
-                  o = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c));
-                } else {
-                  o = f2fma(DT, acc[j], c);
-                }
-                const int rr = ry + j;
-                ol[j] = (lane_in && rr >= eyl && rr < GH - eyl) ? (o & rmask[j]) : 0ull;
-              }
-              if (l == TK - 1) {
-                // ---- last level: u^{n+TK} and u^{n+TK-1} on the output tile ------------------
-                if (q >= zb && q < ze && lane_out && xin0) {
-                  const long long off = (long long)q * plane + rowoff;
-#pragma unroll
-                  for (int j = 0; j < VY; ++j) {
-                    const int rr = ry + j;
-                    if (rr >= HY0 && rr < GH - HY0 && yin[j]) {
-                      const uint64_t pv = ql[TK - 2][md<QN>(u - R)][j];
-                      if (xin1) {
-                        sts64(p.outC + off + j * p.X, ol[j]);
-                        if (WAVE || p.write_prev) sts64(p.outP + off + j * p.X, pv);
-                      } else {
-                        p.outC[off + j * p.X] = lo_of(ol[j]);
-                        if (WAVE || p.write_prev) p.outP[off + j * p.X] = lo_of(pv);
-                      }
-                    }
-                  }
-                }
-              }
-              if (wrec && q >= zb && q < ze && lane_out) {
-#pragma unroll
-                for (int j = 0; j < VY; ++j)
-                  if (yin[j] && ry + j >= HY0 && ry + j < GH - HY0)
-                    sample_receivers_row(ol[j], p, q, y0 + j, x0, p.tr_step + l);
-              }
-            }
-            mbar_arrive(&le[lslot_r]);
-          }
-          if (l < TK - 1) {
-#pragma unroll
-            for (int j = 0; j < VY; ++j) ql[l < NL ? l : 0][u][j] = ol[j];
-          }
-        }
-        // advance ring counters (the level rings of every level share the step schedule)
-        if (++lslot_w == DL) { lslot_w = 0; lph_w ^= 1u; }
-        if (a >= R) { if (++lslot_r == DL) { lslot_r = 0; lph_r ^= 1u; } }
-        if (WAVE && ++e_use == PD + 1) e_use = 0;
-        if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
-      }
-    }
-  }
-  if (WAVE) cp_async_wait<0>();
+  for (int m = 1; m < TK; ++m) l += (warp >= G::wbase(m)) ? 1 : 0;
+  dispatch_level<0, R, TK, WAVE, OY>(l, p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
 }
 
 }  // namespace st

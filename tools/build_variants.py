@@ -1,4 +1,7 @@
-"""Build experimental variants of the untiled kernel for a config sweep (see tools/sweep_variants.sh)."""
+"""Build experimental variants of the sweep kernels for a config sweep (see tools/gpu_variants.sh).
+
+    python tools/build_variants.py NAME [NAME ...]
+"""
 import concurrent.futures as cf
 import os
 import sys
@@ -6,15 +9,13 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1707_02347_b200.build import build_variant  # noqa: E402
 
-ONLY = [(3, 1, 6, 1), (3, 1, 4, 1), (3, 1, 8, 1)]
+ONLY = [(3, 1, 6, 1), (3, 1, 4, 1), (3, 1, 8, 1), (3, 1, 4, 2), (3, 0, 1, 1), (3, 0, 1, 2)]
 VARIANTS = {
-    "base": dict(defines=[], ncw=16),
-    "pd6": dict(defines=["-DST_PD=6"], ncw=16),
-    "d8": dict(defines=["-DST_T1_DEPTH=8"], ncw=16),
-    "d4": dict(defines=["-DST_T1_DEPTH=4"], ncw=16),
-    "ncw20": dict(defines=[], ncw=20),
-    "ncw24": dict(defines=[], ncw=24),
-    "ncw12": dict(defines=[], ncw=12),
+    "base": dict(defines=[]),
+    "rot": dict(defines=["-DST_ROT1=1", "-DST_ROT2=1"]),
+    "rot1": dict(defines=["-DST_ROT1=1"]),
+    "rot2": dict(defines=["-DST_ROT2=1"]),
+    "rot_pd3": dict(defines=["-DST_ROT1=1", "-DST_ROT2=1", "-DST_PD2=3"]),
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)

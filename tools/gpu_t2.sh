@@ -4,7 +4,7 @@ set -u
 MODE=${1:-}
 O=gpurun_out; mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "ragged or tiny or composition or C1 or C2" > $O/t2_pytest.log 2>&1; echo "exit $?" >> $O/t2_pytest.log
-for c in "C3 --tk 2" "C3 --tk 1" "C2 --tk 1" "C2 --tk 2" "C2 --tk 4" "C2 --tk 8"; do
+for c in "C3 --tk 2" "C2 --tk 2" "C2 --tk 4"; do
   set -- $c
   timeout 300 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/t2_bench_$1_$3.json 2> $O/t2_bench_$1_$3.err
 done
