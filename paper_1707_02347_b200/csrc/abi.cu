@@ -163,20 +163,28 @@ __global__ void swap_kernel(float4* __restrict__ a, float4* __restrict__ b, long
 }
 
 // ------------------------------------------------------------------ tensor maps
-st_status encode_map(stencil_plan* p, const st::KernelEntry* k, const float* field, CUtensorMap* map) {
+// 3-D fp32 map over the valid planes of a [Z][rows][row_elems]-strided array: dims (dim0, ny,
+// valid planes), box (box_w, box_h, 1); out-of-bounds boxes are zero-filled (Dirichlet halo).
+st_status encode_box(stencil_plan* p, const float* base, long long dim0, long long row_elems,
+                     long long plane_elems, int box_w, int box_h, CUtensorMap* map) {
   const long long zv_lo = p->G - (p->has_lo ? p->G : 0);
   const long long zv_hi = p->G + p->nzl + (p->has_hi ? p->G : 0);
-  void* base = const_cast<float*>(field + zv_lo * p->X * p->Y);
-  cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)(zv_hi - zv_lo)};
-  cuuint64_t strides[2] = {(cuuint64_t)(p->X * 4), (cuuint64_t)(p->X * p->Y * 4)};
-  cuuint32_t box[3] = {(cuuint32_t)k->bw, (cuuint32_t)k->bh, 1};
+  void* b = const_cast<float*>(base + zv_lo * plane_elems);
+  cuuint64_t dims[3] = {(cuuint64_t)dim0, (cuuint64_t)p->ny, (cuuint64_t)(zv_hi - zv_lo)};
+  cuuint64_t strides[2] = {(cuuint64_t)(row_elems * 4), (cuuint64_t)(plane_elems * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = p->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+  CUresult r = p->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, b, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(p, ST_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
   return ST_OK;
+}
+
+// u^n box with halo of instance k over a field
+st_status encode_map(stencil_plan* p, const st::KernelEntry* k, const float* field, CUtensorMap* map) {
+  return encode_box(p, field, p->nx, p->X, p->X * p->Y, k->bw, k->bh, map);
 }
 
 // choose ring depth / occupancy for one instance
@@ -497,8 +505,11 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
   // buffers: 0 = caller P, 1 = caller C, 2 = scratch P2, 3 = scratch C2
   float* bufs[4] = {u_prev, u_cur, static_cast<float*>(p->p2.ptr), static_cast<float*>(p->c2.ptr)};
   int prev = 0, cur = 1;
-  CUtensorMap maps_t1[4], maps_tk[4];
+  CUtensorMap maps_t1[4], maps_tk[4], maps_p0[4], maps_u1[4], map_a0, map_a1;
   bool have_t1[4] = {false, false, false, false}, have_tk[4] = {false, false, false, false};
+  bool have_p0[4] = {false, false, false, false}, have_u1[4] = {false, false, false, false};
+  bool have_ac = false;
+  st::KernelMaps km{};
 
   st::SweepParams sp{};
   sp.nx = (int)p->nx; sp.ny = (int)p->ny; sp.X = (int)p->X; sp.plane = plane;
@@ -528,6 +539,27 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
       if (s != ST_OK) return s;
       have[cur] = true;
     }
+    km.u = maps[cur];
+    if (k->ebw > 0) {   // producer-streamed u^{n-1}, u^n and medium boxes (time-tiled wave)
+      if (!have_ac) {
+        const float* acf = static_cast<const float*>(p->ac.ptr);
+        s = encode_box(p, acf, 2 * p->X, 2 * p->X, 2 * plane, 128, k->eh0, &map_a0);
+        if (s == ST_OK) s = encode_box(p, acf, 2 * p->X, 2 * p->X, 2 * plane, 128, k->eh1, &map_a1);
+        if (s != ST_OK) return s;
+        have_ac = true;
+      }
+      if (!have_p0[prev]) {
+        s = encode_box(p, bufs[prev], p->nx, p->X, plane, k->ebw, k->eh0, &maps_p0[prev]);
+        if (s != ST_OK) return s;
+        have_p0[prev] = true;
+      }
+      if (!have_u1[cur]) {
+        s = encode_box(p, bufs[cur], p->nx, p->X, plane, k->ebw, k->eh1, &maps_u1[cur]);
+        if (s != ST_OK) return s;
+        have_u1[cur] = true;
+      }
+      km.p0 = maps_p0[prev]; km.a0 = map_a0; km.u1 = maps_u1[cur]; km.a1 = map_a1;
+    }
     // output plane range after j+steps of the nt steps covered by the ghost zones
     const long long shrink = (long long)(nt - j - steps) * c.radius;
     sp.out_lo = (int)(p->has_lo ? p->G - shrink : p->G);
@@ -554,7 +586,7 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
     const int chunks = choose_chunks(p, k, bps, tiles, planes);
     sp.zchunk = (int)((planes + chunks - 1) / chunks);
     dim3 grid((unsigned)((p->nx + k->ox - 1) / k->ox), (unsigned)((p->ny + k->oy - 1) / k->oy), (unsigned)chunks);
-    CK(k->launch(maps[cur], sp, grid, nslot, smem, p->stream), "sweep kernel launch");
+    CK(k->launch(km, sp, grid, nslot, smem, p->stream), "sweep kernel launch");
     ++launches;
     tiled_launches += tiled ? 1 : 0;
     prev = new_prev; cur = new_cur;

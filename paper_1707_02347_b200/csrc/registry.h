@@ -14,7 +14,7 @@
 
 namespace st {
 
-typedef cudaError_t (*launch_fn)(const CUtensorMap& map, const SweepParams& p, dim3 grid,
+typedef cudaError_t (*launch_fn)(const KernelMaps& maps, const SweepParams& p, dim3 grid,
                                  int nslot, size_t smem, cudaStream_t stream);
 typedef cudaError_t (*attr_fn)(size_t smem, cudaFuncAttributes* attr, int* blocks_per_sm,
                                int nthreads);
@@ -30,6 +30,8 @@ struct KernelEntry {
   launch_fn launch;
   attr_fn query;       // sets max dynamic smem, returns attributes and occupancy
   int extra_depth;     // preferred ring prefetch depth beyond the rz+1 resident planes
+  int ebw = 0, eh0 = 0, eh1 = 0;   // time-tiled kernel (wave): field box width, level-0 / level-1
+                                   // box rows of the producer-streamed u^{n-1}, u^n, medium
 };
 
 // Defined in the generated instance translation units.
@@ -38,9 +40,9 @@ const KernelEntry* registry_end();
 const KernelEntry* find_kernel(int ndim, int time_order, int radius, int tk);
 
 template <int R, int TK, bool WAVE, int NDIM, int VY, int NWY>
-cudaError_t launch_sweep(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
+cudaError_t launch_sweep(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                          size_t smem, cudaStream_t stream) {
-  sweep_kernel<R, TK, WAVE, NDIM, VY, NWY><<<grid, 32 * NWY, smem, stream>>>(map, p, nslot);
+  sweep_kernel<R, TK, WAVE, NDIM, VY, NWY><<<grid, 32 * NWY, smem, stream>>>(maps.u, p, nslot);
   return cudaGetLastError();
 }
 
@@ -69,9 +71,9 @@ constexpr KernelEntry make_entry() {
 
 // ---- warp-specialised untiled kernel (sweep1.cuh)
 template <int R, bool WAVE, int NDIM, int NCW>
-cudaError_t launch_sweep1(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
+cudaError_t launch_sweep1(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  sweep1_kernel<R, WAVE, NDIM, NCW><<<grid, 32 * (NCW + 1), smem, stream>>>(map, p, nslot);
+  sweep1_kernel<R, WAVE, NDIM, NCW><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
   return cudaGetLastError();
 }
 
@@ -98,9 +100,9 @@ constexpr KernelEntry make_entry1() {
 
 // ---- warp-specialised time-tiled kernel (sweep2.cuh): one warp group per level
 template <int R, int TK, bool WAVE, int OY>
-cudaError_t launch_sweep2(const CUtensorMap& map, const SweepParams& p, dim3 grid, int nslot,
+cudaError_t launch_sweep2(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  sweep2_kernel<R, TK, WAVE, OY><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(map, p, nslot);
+  sweep2_kernel<R, TK, WAVE, OY><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(maps, p, nslot);
   return cudaGetLastError();
 }
 
@@ -126,7 +128,8 @@ constexpr KernelEntry make_entry2() {
   using G = Geom2<R, TK, WAVE, OY>;
   return KernelEntry{3, WAVE ? 2 : 1, R, TK, 2, G::NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      R, (size_t)G::SLOT_BYTES, (size_t)G::FIXED_BYTES,
-                     &launch_sweep2<R, TK, WAVE, OY>, &query_sweep2<R, TK, WAVE, OY>, ST_T2_DEPTH};
+                     &launch_sweep2<R, TK, WAVE, OY>, &query_sweep2<R, TK, WAVE, OY>, ST_T2_DEPTH,
+                     WAVE ? G::EBW : 0, WAVE ? G::GH : 0, WAVE ? G::OY : 0};
 }
 
 }  // namespace st

@@ -55,6 +55,13 @@ struct SweepParams {
   int tr_step;                // run-relative step index of level 0 of this pass
 };
 
+// Tensor maps of one launch: u = u^n box with halo (every kernel); the time-tiled kernel's
+// producer also streams p0 = u^{n-1} and a0 = medium for level 0, u1 = u^n and a1 = medium for
+// level 1 (boxes without halo).
+struct KernelMaps {
+  CUtensorMap u, p0, a0, u1, a1;
+};
+
 // ------------------------------------------------------------------ packed fp32x2 (FTZ) ops
 __device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
   uint64_t r; asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r;

@@ -18,8 +18,9 @@
 //     rows in a register queue of 2r+1 planes and takes the x/y neighbours from the centre plane
 //     in shared memory.  Levels below TK-1 publish every plane into their own ring; the last
 //     level writes u^{n+TK}, u^{n+TK-1} to global memory.
-//   * u^{n-1} (level 0), u^n (level 1) and the medium of each level's plane are staged PD steps
-//     ahead with cp.async (wave; the medium a, c is read once per level, from L2 after level 0).
+//   * the producer also streams, per step, u^{n-1} and the medium of level 0's plane and u^n and
+//     the medium of level 1's plane (wave) as TMA boxes into two more mbarrier rings, so the
+//     consumer warps never touch global memory except for the final stores.
 // All shared-memory traffic uses 32-bit shared-window addresses.  Arithmetic is the canonical
 // per-point order of include/stencil.h, so every value is bit-identical to the untiled sweep and
 // to the CPU oracle (oracle/, never included here).
@@ -102,21 +103,31 @@ struct Geom2 {
 #endif
   static constexpr int DL = R + ST_DL2;            // level-ring depth (planes); >= R + 1 needed
   static constexpr int LVL_BYTES = GW * (GH + 2 * R) * 4;   // one plane + R pad rows each side
-#ifndef ST_PD2
-#define ST_PD2 2
+#ifndef ST_DE2
+#define ST_DE2 3
 #endif
-  static constexpr int PD = ST_PD2;                // cp.async staging distance (steps)
-  // staging entry (wave): [2 rows x 64: u^{n-1} (level 0) or u^n (level 1)][2 rows x 128: a, c]
-  static constexpr int STAGE_BYTES = WAVE ? (2 * 64 + 2 * 128) * 4 : 0;
-  static constexpr int BAR_BYTES = 2048;           // full[64] | empty[64] | lfull[TK-1][DL] | lempty[TK-1][DL]
+#ifndef ST_ROT2
+#define ST_ROT2 1
+#endif
+  // producer-streamed boxes (wave): level 0 gets u^{n-1} and the medium of its plane (GH rows),
+  // level 1 gets u^n and the medium of its plane (OY rows); DE entries per ring.
+  static constexpr int DE = ST_DE2;
+  static constexpr int XSE = HX0 % 4;              // keep the field box start 16-B aligned
+  static constexpr int EBW = GW + (XSE ? 4 : 0);   // field box width (floats)
+  // field part first (padded to 128 B: TMA destinations are 128-B aligned), then the medium
+  static constexpr int E0_FIELD = (EBW * GH * 4 + 127) / 128 * 128, E0_BYTES = E0_FIELD + 128 * GH * 4;
+  static constexpr int E1_FIELD = (EBW * OY * 4 + 127) / 128 * 128, E1_BYTES = E1_FIELD + 128 * OY * 4;
+  static constexpr int BAR_BYTES = 2048;   // full[64] | empty[64] | lfull | lempty | E0 f/e | E1 f/e
+  static constexpr int EBAR_OFF = 1792;
   static constexpr int LRING_OFF = BAR_BYTES;
-  static constexpr int STAGE_OFF = LRING_OFF + (TK - 1) * DL * LVL_BYTES;
-  static constexpr int FIXED_BYTES = STAGE_OFF + NCW * (PD + 1) * STAGE_BYTES;
+  static constexpr int E0_OFF = LRING_OFF + (TK - 1) * DL * LVL_BYTES;
+  static constexpr int E1_OFF = E0_OFF + (WAVE ? DE * E0_BYTES : 0);
+  static constexpr int FIXED_BYTES = E1_OFF + (WAVE ? DE * E1_BYTES : 0);
+  static_assert(1024 + 16 * (TK - 1) * DL <= EBAR_OFF && EBAR_OFF + 32 * DE <= BAR_BYTES, "barrier area");
   static_assert(TK >= 2 && (!WAVE || TK == 2), "time-tiled kernel: wave TK = 2, heat TK >= 2");
   static_assert(OY % 2 == 0 && NCW + 1 <= 32, "warp budget");
   static_assert(OX > 0, "tile too small for this radius / depth");
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
-  static_assert(8 * (128 + 2 * (TK - 1) * DL) <= BAR_BYTES, "barrier area");
   static_assert(FIXED_BYTES % 128 == 0, "TMA ring alignment");
 };
 
@@ -125,13 +136,14 @@ struct Geom2 {
 // centre is q[R].
 template <int R, int PB>
 __device__ __forceinline__ void accum2(uint64_t (&acc)[2], const uint64_t (&q)[2 * R + 1][2],
-                                       uint32_t cb, const SweepParams& p) {
+                                       uint32_t cb, const SweepParams& p, const int CI) {
   constexpr int RX2 = (R + 1) & ~1;
+  constexpr int QN = 2 * R + 1;
   const uint64_t K0 = splat(p.K0);
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const uint32_t rb = cb + j * PB;
-    const uint64_t c = q[R][j];
+    const uint64_t c = q[CI][j];
     uint64_t A[RX2 + 1];
 #pragma unroll
     for (int m = -RX2 / 2; m <= RX2 / 2; ++m) {
@@ -149,10 +161,10 @@ __device__ __forceinline__ void accum2(uint64_t (&acc)[2], const uint64_t (&q)[2
         sx = pack2(fadd_ftz(hi_of(Lm), hi_of(R0)), fadd_ftz(lo_of(L0), lo_of(Rp)));
       }
       a = f2fma(splat(p.W[0][k]), sx, a);
-      const uint64_t yl = (j - k >= 0) ? q[R][(j - k) >= 0 ? (j - k) : 0] : ld_s64r(rb - k * PB);
-      const uint64_t yr = (j + k < 2) ? q[R][(j + k) < 2 ? (j + k) : 0] : ld_s64r(rb + k * PB);
+      const uint64_t yl = (j - k >= 0) ? q[CI][(j - k) >= 0 ? (j - k) : 0] : ld_s64r(rb - k * PB);
+      const uint64_t yr = (j + k < 2) ? q[CI][(j + k) < 2 ? (j + k) : 0] : ld_s64r(rb + k * PB);
       a = f2fma(splat(p.W[1][k]), f2add(yl, yr), a);
-      a = f2fma(splat(p.W[2][k]), f2add(q[R - k][j], q[R + k][j]), a);
+      a = f2fma(splat(p.W[2][k]), f2add(q[md<QN>(CI - k)][j], q[md<QN>(CI + k)][j]), a);
     }
     acc[j] = a;
   }
@@ -164,9 +176,11 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
                                            const int warp, const int lane, const int tx0,
                                            const int ty0, const int zb, const int ze) {
   using G = Geom2<R, TK, WAVE, OY>;
-  constexpr int QN = G::QN, GW = G::GW, BW = G::BW, DL = G::DL, PD = G::PD, GH = G::GH;
+  constexpr int QN = G::QN, GW = G::GW, BW = G::BW, DL = G::DL, DE = G::DE, GH = G::GH;
   constexpr int HX0 = G::HX0, HY0 = (TK - 1) * R;
-  constexpr int SLOT = G::SLOT_BYTES, LVL = G::LVL_BYTES, STB = G::STAGE_BYTES;
+  constexpr int SLOT = G::SLOT_BYTES, LVL = G::LVL_BYTES;
+  constexpr int EB = (L == 0) ? G::E0_BYTES : G::E1_BYTES;            // E-ring entry
+  constexpr int EFIELD = (L == 0) ? G::E0_FIELD : G::E1_FIELD;        // medium part offset
   constexpr int PB = (L == 0) ? BW * 4 : GW * 4;   // input-plane row pitch (bytes)
   const int wl = warp - G::wbase(L);
   const int r0 = L * R + 2 * wl;                    // region row of my first row
@@ -207,32 +221,14 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
   const uint32_t ring_out = sbase + G::LRING_OFF + (L < TK - 1 ? L : 0) * DL * LVL;
   const uint32_t my_in = (L == 0) ? ((r0 + R) * BW + G::BCOL + 2 * lane) * 4 : ((r0 + R) * GW + 2 * lane) * 4;
   const uint32_t my_out = ((r0 + R) * GW + 2 * lane) * 4;
-  const uint32_t stage = sbase + G::STAGE_OFF + warp * (PD + 1) * STB;
-
-  // ---- staging (wave): level 0: u^{n-1}, a/c of its plane; level 1: u^n, a/c of its plane ----
+  // E ring (wave): level 0 reads ring E0 (rows = region rows), level 1 ring E1 (rows from R)
+  const uint32_t e_base = sbase + ((L == 0) ? G::E0_OFF : G::E1_OFF);
+  const uint32_t e_full = sbase + G::EBAR_OFF + ((L == 0) ? 0 : 16 * DE), e_empty = e_full + 8 * DE;
+  const int er = r0 - L * R;                         // my first row inside the E box
+  const uint32_t my_ef = (er * G::EBW + G::XSE + 2 * lane) * 4;      // field pair, row er
+  const uint32_t my_ea = EFIELD + (er * 128 + 4 * lane) * 4;          // medium float4, row er
   const long long plane = p.plane;
-  const float* gsrc = (L == 0) ? p.P : p.C;
-  long long soff = (long long)(p_first - (L + 1) * R) * plane + (long long)y0 * p.X + x0;
   const int X = p.X;
-  int a_iss = 0, e_iss = 0, e_use = 0;
-  auto stage_next = [&]() {
-    if (xin0 && a_iss >= a_lo && a_iss < a_hi) {
-      const uint32_t e = stage + e_iss * STB;
-      const float* g = gsrc + soff;
-      const float4* ga = p.ac + (soff >> 1);
-      if (yin0) { cp_async8_s(e + 8 * lane, g); cp_async16_s(e + 512 + 16 * lane, ga); }
-      if (yin1) { cp_async8_s(e + 256 + 8 * lane, g + X); cp_async16_s(e + 1024 + 16 * lane, ga + (X >> 1)); }
-    }
-    cp_async_commit();
-    ++a_iss;
-    soff += plane;
-    if (++e_iss == PD + 1) e_iss = 0;
-  };
-  if (WAVE) {
-#pragma unroll 1
-    for (int i = 0; i < PD; ++i) stage_next();
-  }
-
   uint64_t q[QN][2];
 #pragma unroll
   for (int i = 0; i < QN; ++i) q[i][0] = q[i][1] = 0ull;
@@ -241,48 +237,58 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
   int in_slot = 0;  uint32_t in_ph = 0;            // input slot of step a
   int c_slot = (L == 0) ? (R % nslot) : 0;         // centre slot (TMA: arrival a-R; ring: step a-R)
   int out_slot = 0; uint32_t out_ph = 0;           // output ring slot of step a
+  int e_slot = 0; uint32_t e_ph = 0;               // E-ring entry of step a
   const uint64_t DT = splat(p.dt);
   const bool wr_prev = WAVE || p.write_prev;
   const long long obase = (long long)(p_first - TK * R) * plane + (long long)y0 * X + x0;
 
+  // ST_ROT2 = 1: the z-queue is rotated by register moves after each step (code = one step
+  // body); 0: the loop is unrolled by the queue length and the queue indexed modulo QN.
+  constexpr int UNR = ST_ROT2 ? 1 : QN;
 #pragma unroll 1
-  for (int a = 0; a < n_arr; ++a) {
+  for (int base = 0; base < n_arr; base += UNR) {
+#pragma unroll
+  for (int uu = 0; uu < UNR; ++uu) {
+    const int a = base + uu;
+    if (a >= n_arr) break;
+    const int iN = ST_ROT2 ? QN - 1 : uu;            // queue index of the newest plane
+    const int iC = ST_ROT2 ? R : md<QN>(uu - R);     // queue index of the centre plane
     // ---- input plane of step a into the queue ----------------------------------------------
     if (L == 0) {
       mb_wait(b_full + 8 * in_slot, in_ph);
       const uint32_t s = ring_in + in_slot * SLOT + my_in;
-      q[QN - 1][0] = ld_s64<0>(s);
-      q[QN - 1][1] = ld_s64<PB>(s);
+      q[iN][0] = ld_s64<0>(s);
+      q[iN][1] = ld_s64<PB>(s);
       if (a < R) mb_arrive(b_empty + 8 * in_slot);   // never a centre plane
       if (++in_slot == nslot) { in_slot = 0; in_ph ^= 1u; }
     } else {
       mb_wait(lf_in + 8 * in_slot, in_ph);
       const uint32_t s = ring_in + in_slot * LVL + my_in;
-      q[QN - 1][0] = ld_s64<0>(s);
-      q[QN - 1][1] = ld_s64<PB>(s);
+      q[iN][0] = ld_s64<0>(s);
+      q[iN][1] = ld_s64<PB>(s);
       if (++in_slot == DL) { in_slot = 0; in_ph ^= 1u; }
     }
-    if (WAVE) stage_next();
+    // ---- this step's E entry (wave) ----------------------------------------------------------
+    if (WAVE) mb_wait(e_full + 8 * e_slot, e_ph);
 
     // ---- level L at plane p_first + a - (L+1)R ----------------------------------------------
     uint64_t o0 = 0ull, o1 = 0ull;
     const bool centre = (L == 0) ? (a >= 2 * R) : (a >= R);
     if (centre) {
       if (a >= a_lo && a < a_hi) {
-        if (WAVE) cp_async_wait<PD>();              // this step's staged group has landed
         const int qp = p_first + a - (L + 1) * R;
         const uint32_t cb = ring_in + c_slot * ((L == 0) ? SLOT : LVL) + my_in;
         uint64_t acc[2];
-        accum2<R, PB>(acc, q, cb, p);
+        accum2<R, PB>(acc, q, cb, p, iC);
         if (wsrc) {
           if (yin0) acc[0] = add_sources_row(acc[0], p, qp, y0, x0, p.wl_step + L);
           if (yin1) acc[1] = add_sources_row(acc[1], p, qp, y0 + 1, x0, p.wl_step + L);
         }
-        const uint64_t c0 = q[R][0], c1 = q[R][1];
+        const uint64_t c0 = q[iC][0], c1 = q[iC][1];
         if (WAVE) {
-          const uint32_t e = stage + e_use * STB;
-          const uint64_t p0 = ld_s64r(e + 8 * lane), p1 = ld_s64r(e + 256 + 8 * lane);
-          const float4 a0 = ld_s128(e + 512 + 16 * lane), a1 = ld_s128(e + 1024 + 16 * lane);
+          const uint32_t e = e_base + e_slot * EB;
+          const uint64_t p0 = ld_s64r(e + my_ef), p1 = ld_s64r(e + my_ef + G::EBW * 4);
+          const float4 a0 = ld_s128(e + my_ea), a1 = ld_s128(e + my_ea + 128 * 4);
           o0 = f2fma(pack2(a0.z, a0.w), acc[0], f2fma(pack2(a0.x, a0.y), f2sub(p0, c0), c0));
           o1 = f2fma(pack2(a1.z, a1.w), acc[1], f2fma(pack2(a1.x, a1.y), f2sub(p1, c1), c1));
         } else {
@@ -320,7 +326,10 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
         if (++c_slot == DL) c_slot = 0;
       }
     }
-    if (WAVE && ++e_use == PD + 1) e_use = 0;
+    if (WAVE) {
+      mb_arrive(e_empty + 8 * e_slot);
+      if (++e_slot == DE) { e_slot = 0; e_ph ^= 1u; }
+    }
 
     // ---- publish level L's plane into its ring (levels below the last) -----------------------
     if (L < TK - 1) {
@@ -333,10 +342,12 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
     }
 
     // ---- rotate the z-queue -------------------------------------------------------------------
+    if (ST_ROT2) {
 #pragma unroll
-    for (int i = 0; i + 1 < QN; ++i) { q[i][0] = q[i + 1][0]; q[i][1] = q[i + 1][1]; }
+      for (int i = 0; i + 1 < QN; ++i) { q[i][0] = q[i + 1][0]; q[i][1] = q[i + 1][1]; }
+    }
   }
-  if (WAVE) cp_async_wait<0>();
+  }
 }
 
 template <int L, int R, int TK, bool WAVE, int OY>
@@ -351,10 +362,10 @@ __device__ __forceinline__ void dispatch_level(int l, const SweepParams& p, int 
 
 template <int R, int TK, bool WAVE, int OY>
 __global__ void __launch_bounds__(Geom2<R, TK, WAVE, OY>::NTHREADS, 1)
-sweep2_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
+sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ SweepParams p,
               const int nslot) {
   using G = Geom2<R, TK, WAVE, OY>;
-  constexpr int NCW = G::NCW, DL = G::DL;
+  constexpr int NCW = G::NCW, DL = G::DL, DE = G::DE;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t sbase = smem_u32(smem);
   const int tid = threadIdx.x;
@@ -374,25 +385,55 @@ sweep2_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
         mb_init(sbase + 1024 + 8 * (l * DL + i), 32 * G::warps(l));                         // writers
         mb_init(sbase + 1024 + 8 * ((TK - 1) * DL + l * DL + i), 32 * G::warps(l + 1));     // readers
       }
+    if (WAVE)
+      for (int i = 0; i < DE; ++i) {
+        mb_init(sbase + G::EBAR_OFF + 8 * i, 1);                        // E0 full (expect_tx)
+        mb_init(sbase + G::EBAR_OFF + 8 * (DE + i), 32 * G::warps(0));  // E0 empty
+        mb_init(sbase + G::EBAR_OFF + 8 * (2 * DE + i), 1);             // E1 full
+        mb_init(sbase + G::EBAR_OFF + 8 * (3 * DE + i), 32 * G::warps(1));
+      }
     fence_mbar_init();
   }
   __syncthreads();
 
   if (warp == NCW) {
     // ------------------------------------------------------------------ producer warp
+    // lane 0 streams the u^n ring, lane 1 (wave) the E rings: the two streams run ahead of their
+    // consumers independently (each bounded by its own ring depth).
+    const int p_first = zb - TK * R, n_arr = (ze - zb) + 2 * TK * R;
+    const int gx = tx0 - G::HX0, gy = ty0 - (TK - 1) * R;
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmapC)) : "memory");
-      const int p_first = zb - TK * R, n_arr = (ze - zb) + 2 * TK * R;
-      const int gx = tx0 - G::HX0, gy = ty0 - (TK - 1) * R;
+      asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&maps.u)) : "memory");
       const uint32_t ring = sbase + G::FIXED_BYTES;
       int slot = 0;
       uint32_t ph = 0;
       for (int a = 0; a < n_arr; ++a) {
         if (a >= nslot) mb_wait(sbase + 512 + 8 * slot, ph ^ 1u);
         mb_expect_tx(sbase + 8 * slot, (uint32_t)(G::BW * G::BH * 4));
-        tma_load_3d_s(ring + slot * G::SLOT_BYTES, &tmapC, sbase + 8 * slot, gx - G::BCOL, gy - R,
+        tma_load_3d_s(ring + slot * G::SLOT_BYTES, &maps.u, sbase + 8 * slot, gx - G::BCOL, gy - R,
                       p_first + a - p.zv_lo);
         if (++slot == nslot) { slot = 0; ph ^= 1u; }
+      }
+    } else if (WAVE && lane == 1) {
+      const uint32_t ebar = sbase + G::EBAR_OFF;
+      int es = 0;
+      uint32_t eph = 0;
+      for (int a = 0; a < n_arr; ++a) {
+        // level 0 plane s = p_first + a - R (rows gy..), level 1 plane s - R (rows gy + R..)
+        const int zs = p_first + a - R - p.zv_lo;
+        if (a >= DE) {
+          mb_wait(ebar + 8 * (DE + es), eph ^ 1u);
+          mb_wait(ebar + 8 * (3 * DE + es), eph ^ 1u);
+        }
+        const uint32_t f0 = ebar + 8 * es, f1 = ebar + 8 * (2 * DE + es);
+        const uint32_t d0 = sbase + G::E0_OFF + es * G::E0_BYTES, d1 = sbase + G::E1_OFF + es * G::E1_BYTES;
+        mb_expect_tx(f0, (uint32_t)((G::EBW + 128) * G::GH * 4));
+        tma_load_3d_s(d0, &maps.p0, f0, gx - G::XSE, gy, zs);
+        tma_load_3d_s(d0 + G::E0_FIELD, &maps.a0, f0, 2 * gx, gy, zs);
+        mb_expect_tx(f1, (uint32_t)((G::EBW + 128) * G::OY * 4));
+        tma_load_3d_s(d1, &maps.u1, f1, gx - G::XSE, gy + R, zs - R);
+        tma_load_3d_s(d1 + G::E1_FIELD, &maps.a1, f1, 2 * gx, gy + R, zs - R);
+        if (++es == DE) { es = 0; eph ^= 1u; }
       }
     }
     return;

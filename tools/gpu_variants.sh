@@ -5,7 +5,7 @@ O=gpurun_out; mkdir -p $O
 for v in "$@"; do
   export ST_LIB=paper_1707_02347_b200/_varlib/libstencil_$v.so
   timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "ragged or tiny or composition" > $O/v_${v}_pytest.log 2>&1; echo "exit $?" >> $O/v_${v}_pytest.log
-  for c in "C5 --tk 1 --nt 400" "C3 --tk 1 --nt 200" "C3 --tk 2 --nt 200" "C4 --tk 1 --nt 100" "C2 --tk 1" "C2 --tk 2"; do
+  for c in ${CFGS:-"C3 --tk 2 --nt 200" "C2 --tk 2" "C2 --tk 4"}; do
     set -- $c
     timeout 300 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/v_${v}_$1_$3.json 2>$O/v_${v}_$1_$3.err
     python -c "import json;d=json.load(open('$O/v_${v}_$1_$3.json'));print('$v','$1','tk$3',d['value'],d['roofline']['frac'],d['clocks']['sm_mhz'])" >> $O/v_summary.txt 2>/dev/null || echo "$v $1 tk$3 FAILED" >> $O/v_summary.txt
