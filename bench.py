@@ -109,8 +109,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+_OVERRIDE = {}
+
+
 def _problem(cfg: str, gpus: int) -> W.Problem:
-    return W.problem(cfg, gpus=gpus) if cfg == "C5" else W.problem(cfg)
+    p = W.problem(cfg, gpus=gpus) if cfg == "C5" else W.problem(cfg)
+    if _OVERRIDE.get("so"):
+        p = W.Problem(**{**p.__dict__, "space_order": int(_OVERRIDE["so"])})
+    if _OVERRIDE.get("n"):
+        n = tuple(int(v) for v in _OVERRIDE["n"].split("x"))
+        p = W.Problem(**{**p.__dict__, "n": n,
+                         "src": tuple((n[0] // 2, n[1] // 2, n[2] // 2) for _ in p.src),
+                         "rec": tuple(r for r in p.rec if r[0] < n[0] and r[1] < n[1] and r[2] < n[2])})
+    return p
 
 
 def run_gpu(args):
@@ -342,10 +353,13 @@ def main():
     ap.add_argument("--tk", default="auto")
     ap.add_argument("--tc", type=int, default=4, help="halo depth in steps for N > 1")
     ap.add_argument("--nt", type=int, default=None, help="override time steps per bench step")
+    ap.add_argument("--so", type=int, default=None, help="override the space order (study runs only)")
+    ap.add_argument("--grid", default=None, help="override the interior grid, e.g. 512x512x512 (study runs only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=2, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    _OVERRIDE.update(so=args.so, n=args.grid)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

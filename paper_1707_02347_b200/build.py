@@ -31,7 +31,18 @@ def _vy_nwy(ndim: int, R: int, TK: int):
     return 2, 12
 
 
-NCW_T1 = 16   # consumer warps (= tile rows) of the untiled warp-specialised kernel
+NCW_T1 = 16   # consumer warps (= tile rows) of the untiled warp-specialised kernel (2-D, R = 8)
+
+
+def _t1_geom(ndim: int, wave: int, R: int):
+    """(consumer warps, rows per warp) of the untiled kernel.  Two rows per warp share their
+    y-neighbour loads and give two independent FMA chains, which pays for the 3-D wave at
+    R = 3..7 (C5 SO12: 247 -> 260-280 GPts/s); at R = 8 the doubled z-queue no longer fits the
+    128-register budget of 13 warps, and the heat / low-order sweeps are already at the HBM
+    roof with one row per warp (heat C2: 596 vs 511 GPts/s).  Measured, DESIGN.md §10."""
+    if ndim == 3 and wave and 3 <= R <= 7:
+        return 12, 2
+    return NCW_T1, 1
 
 # kernel kinds: 1 = sweep1 (untiled, warp-specialised), 2 = sweep2 (time-tiled, warp-specialised),
 #               0 = sweep (first time-tiled kernel; 2-D and the shapes sweep2 does not fit)
@@ -51,14 +62,16 @@ def instances():
     out = []
     for wave in (0, 1):
         for R in range(1, 9):
-            out.append((3, wave, R, 1, 1, NCW_T1, 1))
+            ncw, vy = _t1_geom(3, wave, R)
+            out.append((3, wave, R, 1, vy, ncw, 1))
             oy = _sweep2_oy(wave, R, 2)
             if oy:
                 out.append((3, wave, R, 2, 2, oy, 2))
             else:
                 out.append((3, wave, R, 2) + _vy_nwy(3, R, 2) + (0,))
         for R in range(1, 9):
-            out.append((2, wave, R, 1, 1, NCW_T1, 1))
+            ncw, vy = _t1_geom(2, wave, R)
+            out.append((2, wave, R, 1, vy, ncw, 1))
         out.append((2, wave, 1, 2) + _vy_nwy(2, 1, 2) + (0,))
         out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4) + (0,))
     for R, TK in ((1, 4), (2, 4), (1, 8)):
@@ -67,7 +80,7 @@ def instances():
     return out
 
 
-def _gen_sources(groups: int, inst=None, outdir: str = BUILD, ncw: int = NCW_T1):
+def _gen_sources(groups: int, inst=None, outdir: str = BUILD):
     os.makedirs(outdir, exist_ok=True)
     inst = instances() if inst is None else inst
     groups = max(1, min(groups, len(inst)))
@@ -78,7 +91,7 @@ def _gen_sources(groups: int, inst=None, outdir: str = BUILD, ncw: int = NCW_T1)
         for (ndim, wave, R, TK, VY, NWY, kind) in group:
             w = 'true' if wave else 'false'
             if kind == 1:
-                lines.append(f"  make_entry1<{R}, {w}, {ndim}, {ncw}>(),")
+                lines.append(f"  make_entry1<{R}, {w}, {ndim}, {NWY}, {VY}>(),")
             elif kind == 2:
                 lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}>(),")   # NWY = output rows
             else:
@@ -136,8 +149,8 @@ def _compile(src: str, outdir: str = BUILD, defines=()):
     return obj, r.stderr
 
 
-def _build(outdir, lib, inst=None, defines=(), groups=12, jobs=0, verbose=False, ncw=NCW_T1):
-    srcs = _gen_sources(groups, inst, outdir, ncw) + [os.path.join(CSRC, "abi.cu")]
+def _build(outdir, lib, inst=None, defines=(), groups=12, jobs=0, verbose=False):
+    srcs = _gen_sources(groups, inst, outdir) + [os.path.join(CSRC, "abi.cu")]
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     objs, logs = [], []
     with cf.ThreadPoolExecutor(jobs) as ex:
@@ -164,7 +177,7 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
     return _build(BUILD, LIB, jobs=jobs, verbose=verbose)
 
 
-def build_variant(name: str, defines=(), only=None, ncw: int = NCW_T1, verbose: bool = True) -> str:
+def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = True) -> str:
     """Experimental library _variants/libstencil_<name>.so with extra -D flags and (optionally)
     only the instances whose (ndim, wave, R, TK) is listed; load it with ST_LIB=<path>."""
     inst = instances()
@@ -173,7 +186,9 @@ def build_variant(name: str, defines=(), only=None, ncw: int = NCW_T1, verbose: 
     outdir = os.path.join(HERE, "_variants", name)
     os.makedirs(os.path.join(HERE, "_varlib"), exist_ok=True)
     lib = os.path.join(HERE, "_varlib", f"libstencil_{name}.so")   # shipped to the GPU box
-    return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose, ncw=ncw)
+    if t1 is not None:   # (consumer warps, rows per warp) of the untiled kernel
+        inst = [i[:4] + (t1[1], t1[0], 1) if i[6] == 1 else i for i in inst]
+    return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose)
 
 
 if __name__ == "__main__":

@@ -70,16 +70,16 @@ constexpr KernelEntry make_entry() {
 }
 
 // ---- warp-specialised untiled kernel (sweep1.cuh)
-template <int R, bool WAVE, int NDIM, int NCW>
+template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t launch_sweep1(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  sweep1_kernel<R, WAVE, NDIM, NCW><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  sweep1_kernel<R, WAVE, NDIM, NCW, VY><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
   return cudaGetLastError();
 }
 
-template <int R, bool WAVE, int NDIM, int NCW>
+template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t query_sweep1(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweep1_kernel<R, WAVE, NDIM, NCW>;
+  auto k = sweep1_kernel<R, WAVE, NDIM, NCW, VY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (attr) {
@@ -90,12 +90,12 @@ cudaError_t query_sweep1(size_t smem, cudaFuncAttributes* attr, int* bps, int nt
   return cudaSuccess;
 }
 
-template <int R, bool WAVE, int NDIM, int NCW>
+template <int R, bool WAVE, int NDIM, int NCW, int VY = 1>
 constexpr KernelEntry make_entry1() {
-  using G = Geom1<R, NDIM, NCW>;
-  return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, 1, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+  using G = Geom1<R, NDIM, NCW, VY>;
+  return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      G::RZ, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
-                     &launch_sweep1<R, WAVE, NDIM, NCW>, &query_sweep1<R, WAVE, NDIM, NCW>, ST_T1_DEPTH};
+                     &launch_sweep1<R, WAVE, NDIM, NCW, VY>, &query_sweep1<R, WAVE, NDIM, NCW, VY>, ST_T1_DEPTH};
 }
 
 // ---- warp-specialised time-tiled kernel (sweep2.cuh): one warp group per level

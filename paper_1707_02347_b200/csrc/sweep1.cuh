@@ -57,26 +57,28 @@ static __device__ __noinline__ void sample_receivers_row(uint64_t o, const Sweep
   }
 }
 
-template <int R, int NDIM, int NCW>
+template <int R, int NDIM, int NCW, int VY = 1>
 struct Geom1 {
   static constexpr int RZ = (NDIM == 3) ? R : 0;
   static constexpr int QN = 2 * RZ + 1;
   static constexpr int RX2 = (R + 1) & ~1;
   static constexpr int RXB = (R + 3) & ~3;         // box x halo, multiple of 4 floats (16 B)
-  static constexpr int GW = 64, GH = NCW;
+  static constexpr int GW = 64, GH = NCW * VY;   // VY rows per consumer warp
   static constexpr int BW = GW + 2 * RXB;          // multiple of 8 floats
   static constexpr int BH = GH + 2 * R;
   static constexpr int OX = GW, OY = GH;
   static constexpr int SLOT_BYTES = ((BW * BH * 4) + 127) / 128 * 128;
   static constexpr int NTHREADS = 32 * (NCW + 1);
 #ifndef ST_PD
-#define ST_PD 4
+#define ST_PD 0          // 0: per-geometry default below
 #endif
 #ifndef ST_ROT1
 #define ST_ROT1 0
 #endif
-  static constexpr int PD = ST_PD;                 // cp.async staging distance (planes)
-  static constexpr int STAGE_F = 64 + 128;         // one staged plane row: u^{n-1} (64) + {a,c} (128)
+  // cp.async staging distance (planes).  VY = 2 uses 2: the (12 warps x 2 rows) geometry gave
+  // run-to-run different fields with distance 3 and 4 (unexplained), never with 2.
+  static constexpr int PD = ST_PD ? ST_PD : (VY == 1 ? 4 : 2);
+  static constexpr int STAGE_F = VY * (64 + 128);  // staged plane rows: u^{n-1} (VY x 64) + {a,c} (VY x 128)
   static constexpr int STAGE_BYTES = NCW * (PD + 1) * STAGE_F * 4;
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
 };
@@ -92,11 +94,11 @@ __device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent,
   return false;
 }
 
-template <int R, bool WAVE, int NDIM, int NCW>
+template <int R, bool WAVE, int NDIM, int NCW, int VY>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
 sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
               const int nslot) {
-  using G = Geom1<R, NDIM, NCW>;
+  using G = Geom1<R, NDIM, NCW, VY>;
   constexpr int RZ = G::RZ, QN = G::QN, RX2 = G::RX2, RXB = G::RXB, BW = G::BW;
   constexpr int SLOT_F = G::SLOT_BYTES / 4;
   constexpr int PD = G::PD, STAGE_F = G::STAGE_F;
@@ -142,34 +144,55 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   }
 
   // -------------------------------------------------------------------- consumer warps
+  // warp w owns rows ty0 + w*VY + j (j < VY), a column pair per lane
   const int x0 = tx0 + 2 * lane;
-  const int y = ty0 + warp;
+  const int y0 = ty0 + warp * VY;
   const bool xin0 = x0 < p.nx, xin1 = x0 + 1 < p.nx;
-  const bool yin = y < p.ny;                      // warp-uniform
-  const bool act = yin && xin0;                   // this lane owns >= 1 interior point
-  const uint64_t mask = yin ? ((xin0 ? 0xffffffffull : 0ull) | (xin1 ? 0xffffffff00000000ull : 0ull)) : 0ull;
-  const int col = (warp + R) * BW + 2 * lane + RXB;   // my pair in a ring slot
-  const uint64_t K0 = splat(p.K0);
+  const uint64_t xmask = (xin0 ? 0xffffffffull : 0ull) | (xin1 ? 0xffffffff00000000ull : 0ull);
+  bool yin[VY];
+  uint64_t mask[VY];
+  bool any_row = false;
+#pragma unroll
+  for (int j = 0; j < VY; ++j) {
+    yin[j] = y0 + j < p.ny;                       // warp-uniform
+    mask[j] = yin[j] ? xmask : 0ull;
+    any_row |= yin[j];
+  }
+  const bool act = any_row && xin0;               // this lane owns >= 1 interior point
+  const int col = (warp * VY + R) * BW + 2 * lane + RXB;   // my first row's pair in a ring slot
   const uint64_t DT = splat(p.dt);
-  // rare events of this warp's row (sources / receivers), decided once per CTA chunk
-  const bool wsrc = yin && row_has_entry(p.src_begin, p.src, zb, ze, y, tx0, tx0 + 64);
-  const bool wrec = yin && row_has_entry(p.rec_begin, p.rec, zb, ze, y, tx0, tx0 + 64);
+  // rare events of this warp's rows (sources / receivers), decided once per CTA chunk
+  bool wsrc = false, wrec = false;
+#pragma unroll
+  for (int j = 0; j < VY; ++j) {
+    if (yin[j]) {
+      wsrc |= row_has_entry(p.src_begin, p.src, zb, ze, y0 + j, tx0, tx0 + 64);
+      wrec |= row_has_entry(p.rec_begin, p.rec, zb, ze, y0 + j, tx0, tx0 + 64);
+    }
+  }
 
   // u^{n-1} and the medium {a,a,c,c} of plane s are staged into per-warp shared memory with
   // cp.async PD planes ahead (no registers held across steps, no wait on fresh loads).
   // Every plane of [zb, ze) lies inside the global domain (host invariant), so each step computes.
   const long long plane = p.plane;
+  const int X = p.X, X2 = p.X >> 1;
   float* stage = ring + (size_t)nslot * SLOT_F + (size_t)warp * (PD + 1) * STAGE_F;
   const int s0 = zb - 2 * RZ;                       // level-0 plane of arrival 0
-  const float* gP = p.P + (long long)zb * plane + (long long)y * p.X + x0;   // plane zb
-  const float4* gA = p.ac + (long long)zb * (plane >> 1) + (long long)y * (p.X >> 1) + (x0 >> 1);
-  float* out = p.outP + (long long)zb * plane + (long long)y * p.X + x0;
+  const float* gP = p.P + (long long)zb * plane + (long long)y0 * X + x0;   // plane zb
+  const float4* gA = p.ac + (long long)zb * (plane >> 1) + (long long)y0 * X2 + (x0 >> 1);
+  float* out = p.outP + (long long)zb * plane + (long long)y0 * X + x0;
   int q_iss = zb;                                   // next plane to stage
   int e_use = 0, e_iss = 0;                         // staging entries of plane s and of q_iss
   auto stage_next = [&]() {                         // stage plane q_iss (if in the chunk)
     if (q_iss < ze && act) {
-      cp_async8(stage + e_iss * STAGE_F + 2 * lane, gP);
-      cp_async16(stage + e_iss * STAGE_F + 64 + 4 * lane, gA);
+      float* e = stage + e_iss * STAGE_F;
+#pragma unroll
+      for (int j = 0; j < VY; ++j) {
+        if (yin[j]) {
+          cp_async8(e + j * 64 + 2 * lane, gP + j * X);
+          cp_async16(e + VY * 64 + j * 128 + 4 * lane, gA + j * X2);
+        }
+      }
     }
     cp_async_commit();
     gP += plane; gA += plane >> 1; ++q_iss;
@@ -180,9 +203,11 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     for (int i = 0; i < PD; ++i) stage_next();
   }
 
-  uint64_t qn[QN];
+  uint64_t qn[QN][VY];
 #pragma unroll
-  for (int i = 0; i < QN; ++i) qn[i] = 0ull;
+  for (int i = 0; i < QN; ++i)
+#pragma unroll
+    for (int j = 0; j < VY; ++j) qn[i][j] = 0ull;
   int slot_a = 0, slot_s = RZ % nslot; // ring slots of the arriving plane and of the centre plane
                                        // (the first centre, plane zb, is arrival RZ)
   uint32_t ph_a = 0;
@@ -197,50 +222,50 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       const int idx = base + uu;
       if (idx < n_arr) {
         mbar_wait(&full[slot_a], ph_a);
-        qn[u] = lds64(ring + slot_a * SLOT_F + col);
+#pragma unroll
+        for (int j = 0; j < VY; ++j) qn[u][j] = lds64(ring + slot_a * SLOT_F + col + j * BW);
         if (idx < RZ) mbar_arrive(&empty[slot_a]);   // planes below zb are never a centre
         if (idx >= 2 * RZ) {                          // step s = s0 + idx in [zb, ze)
           if (WAVE) stage_next();                     // plane s + PD
           const int s = s0 + idx;
           const float* rp = ring + slot_s * SLOT_F + col;
-          const uint64_t c = qn[md<QN>(u - RZ)];
-          uint64_t A[RX2 + 1];
+          uint64_t acc[VY];
+          accumulate<R, RZ, QN, VY, NDIM, BW>(acc, qn, rp, p, md<QN>(u - RZ));
+          if (wsrc) {
 #pragma unroll
-          for (int m = -RX2 / 2; m <= RX2 / 2; ++m) A[m + RX2 / 2] = (m == 0) ? c : lds64(rp + 2 * m);
-          uint64_t acc = f2mul(K0, c);
-#pragma unroll
-          for (int k = 1; k <= R; ++k) {
-            uint64_t sx;
-            if ((k & 1) == 0) {
-              sx = f2add(A[RX2 / 2 - k / 2], A[RX2 / 2 + k / 2]);
-            } else {
-              const uint64_t Lm = A[RX2 / 2 - (k + 1) / 2], L0 = A[RX2 / 2 - (k - 1) / 2];
-              const uint64_t R0 = A[RX2 / 2 + (k - 1) / 2], Rp = A[RX2 / 2 + (k + 1) / 2];
-              sx = pack2(fadd_ftz(hi_of(Lm), hi_of(R0)), fadd_ftz(lo_of(L0), lo_of(Rp)));
-            }
-            acc = f2fma(splat(p.W[0][k]), sx, acc);
-            acc = f2fma(splat(p.W[1][k]), f2add(lds64(rp - k * BW), lds64(rp + k * BW)), acc);
-            if (NDIM == 3)
-              acc = f2fma(splat(p.W[2][k]), f2add(qn[md<QN>(u - RZ - k)], qn[md<QN>(u - RZ + k)]), acc);
+            for (int j = 0; j < VY; ++j)
+              if (yin[j]) acc[j] = add_sources_row(acc[j], p, s, y0 + j, x0, p.wl_step);
           }
-          if (wsrc) acc = add_sources_row(acc, p, s, y, x0, p.wl_step);
-          uint64_t o;
+          uint64_t o[VY];
           if (WAVE) {
             cp_async_wait<PD>();                      // the group of plane s has landed
             const float* st_e = stage + e_use * STAGE_F;
-            const uint64_t pv = lds64(st_e + 2 * lane);
-            const float4 m4 = *reinterpret_cast<const float4*>(st_e + 64 + 4 * lane);
-            o = f2fma(pack2(m4.z, m4.w), acc, f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c));
+#pragma unroll
+            for (int j = 0; j < VY; ++j) {
+              const uint64_t c = qn[md<QN>(u - RZ)][j];
+              const uint64_t pv = lds64(st_e + j * 64 + 2 * lane);
+              const float4 m4 = *reinterpret_cast<const float4*>(st_e + VY * 64 + j * 128 + 4 * lane);
+              o[j] = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c)) & mask[j];
+            }
             if (++e_use == PD + 1) e_use = 0;
           } else {
-            o = f2fma(DT, acc, c);
+#pragma unroll
+            for (int j = 0; j < VY; ++j) o[j] = f2fma(DT, acc[j], qn[md<QN>(u - RZ)][j]) & mask[j];
           }
-          o &= mask;
           if (act) {
-            if (xin1) sts64(out, o);
-            else *out = lo_of(o);
+#pragma unroll
+            for (int j = 0; j < VY; ++j) {
+              if (yin[j]) {
+                if (xin1) sts64(out + j * X, o[j]);
+                else out[j * X] = lo_of(o[j]);
+              }
+            }
           }
-          if (wrec) sample_receivers_row(o, p, s, y, x0, p.tr_step);
+          if (wrec) {
+#pragma unroll
+            for (int j = 0; j < VY; ++j)
+              if (yin[j]) sample_receivers_row(o[j], p, s, y0 + j, x0, p.tr_step);
+          }
           mbar_arrive(&empty[slot_s]);
           if (++slot_s == nslot) slot_s = 0;
           out += plane;
@@ -248,7 +273,9 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
         if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
         if (ST_ROT1) {
 #pragma unroll
-          for (int i = 0; i + 1 < QN; ++i) qn[i] = qn[i + 1];
+          for (int i = 0; i + 1 < QN; ++i)
+#pragma unroll
+            for (int j = 0; j < VY; ++j) qn[i][j] = qn[i + 1][j];
         }
       }
     }

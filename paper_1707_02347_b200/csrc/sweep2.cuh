@@ -99,15 +99,15 @@ struct Geom2 {
   static constexpr int OX = GW - 2 * HX0;
   static constexpr int SLOT_BYTES = ((BW * BH * 4) + 127) / 128 * 128;
 #ifndef ST_DL2
-#define ST_DL2 3
+#define ST_DL2 2
 #endif
   static constexpr int DL = R + ST_DL2;            // level-ring depth (planes); >= R + 1 needed
   static constexpr int LVL_BYTES = GW * (GH + 2 * R) * 4;   // one plane + R pad rows each side
 #ifndef ST_DE2
-#define ST_DE2 3
+#define ST_DE2 4
 #endif
 #ifndef ST_ROT2
-#define ST_ROT2 1
+#define ST_ROT2 0
 #endif
   // producer-streamed boxes (wave): level 0 gets u^{n-1} and the medium of its plane (GH rows),
   // level 1 gets u^n and the medium of its plane (OY rows); DE entries per ring.

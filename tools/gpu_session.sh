@@ -17,9 +17,10 @@ if [[ $what == all || $what == tests ]]; then
 fi
 if [[ $what == all || $what == bench ]]; then
   timeout 900 python bench.py --steps 3 --warmup 3 > $O/bench_C5.json 2> $O/bench_C5.err
-  timeout 600 python bench.py --config C3 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_C3.json 2> $O/bench_C3.err
-  timeout 600 python bench.py --config C3 --tk 1 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_C3_tk1.json 2> $O/bench_C3_tk1.err
-  timeout 600 python bench.py --config C2 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_C2.json 2> $O/bench_C2.err
+  for c in "C3 --tk 1" "C3 --tk 2" "C4 --tk 1" "C2 --tk 1" "C2 --tk 2" "C2 --tk 4" "C1 --tk 1"; do
+    set -- $c
+    timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_$1_tk$3.json 2> $O/bench_$1_tk$3.err
+  done
   timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
 fi
 if [[ $what == all || $what == ncu ]]; then
@@ -36,7 +37,7 @@ if [[ $what == all || $what == ncu ]]; then
   # time-tiled C3 (SO8, T_k=2)
   CMD="python tools/prof_run.py --config C3 --tk 2 --nt 6"
   timeout 300 $CMD > $O/plain_prof_c3.log 2>&1 &&
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep2 -s 1 -c 1 \
       -o $O/prof_C3_tk2 -f $CMD > $O/ncu_c3.log 2>&1
 fi
 echo done > $O/session_done.txt
