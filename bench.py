@@ -32,8 +32,12 @@ import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
 
-# Best on-chip time-tile depth per config (measured; DESIGN.md §Measurements)
-AUTO_TK = {"C1": 1, "C2": 4, "C3": 1, "C4": 1, "C5": 1}
+# Best on-chip time-tile depth per config (measured; DESIGN.md §10)
+AUTO_TK = {"C1": 1, "C2": 1, "C3": 1, "C4": 1, "C5": 1, "P256": 1, "P256L": 1, "P384": 1}
+# The paper's own runs of the replica workloads (derived from P:2001-2003 and
+# P:2112-2116): GPts/s over the padded (N+20)^3 array, time-tiled and Devito auto-tuned blocking,
+# on a 4-core i7-6700K.  Context only (another machine, padded-point count).
+PAPER_GPTS = {"P256": (0.921, 0.672), "P256L": (0.818, 0.635), "P384": (0.793, 0.575)}
 METRIC = "GPts/s (grid-point updates/sec)"
 
 
@@ -242,6 +246,15 @@ def run_gpu(args):
                          "per_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src},
             "clocks": ck,
         }
+        if args.config in PAPER_GPTS:
+            tt, blk = PAPER_GPTS[args.config]
+            pad = ((p.n[0] + 8) / p.n[0]) ** 3        # padded (N+20)^3 vs updated (N+12)^3 points
+            out["paper_context"] = {
+                "paper_time_tiled_gpts_padded": tt, "paper_blocked_gpts_padded": blk,
+                "paper_time_tiled_gpts_updated": round(tt / pad, 4),
+                "ratio_vs_paper_time_tiled": round(value / (tt / pad), 1),
+                "paper_hardware": "Intel i7-6700K, 4 cores, icc -O3 (P:1581-1637)",
+                "note": "BASELINE.md derived throughput; different machine and point count"}
     runner.close()
     return out
 

@@ -50,7 +50,7 @@ def _sweep2_oy(wave: int, R: int, TK: int):
     """Output rows of the sweep2 (one warp group per level) instance, or None if it does not fit
     (<= 31 consumer warps of two rows; wave only two levels)."""
     if TK == 2 and R <= 4:
-        return 16 if R < 4 else 14      # <= 20 warps (96 registers/thread) for R = 4
+        return 16 if R < 3 else 14      # <= 20 warps incl. 2 producers (96 registers/thread)
     if not wave and TK == 4 and R <= 2:
         return 8
     return None

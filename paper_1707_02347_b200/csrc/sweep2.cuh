@@ -89,7 +89,8 @@ struct Geom2 {
   static constexpr int warps(int l) { return rows(l) / VY; }
   static constexpr int wbase(int l) { return l == 0 ? 0 : wbase(l - 1) + warps(l - 1); }
   static constexpr int NCW = wbase(TK);            // consumer warps over all levels
-  static constexpr int NTHREADS = 32 * (NCW + 1);
+  static constexpr int NPROD = WAVE ? 2 : 1;       // producer warps: u^n ring (+ E rings, wave)
+  static constexpr int NTHREADS = 32 * (NCW + NPROD);
   static constexpr int RXB = (R + 3) & ~3;
   static constexpr int HX0 = Halo<R, TK>::hx(0);   // level-0 x halo (even)
   static constexpr int XS = HX0 % 4;               // keep the TMA box start 16-B aligned
@@ -104,19 +105,24 @@ struct Geom2 {
   static constexpr int DL = R + ST_DL2;            // level-ring depth (planes); >= R + 1 needed
   static constexpr int LVL_BYTES = GW * (GH + 2 * R) * 4;   // one plane + R pad rows each side
 #ifndef ST_DE2
-#define ST_DE2 4
+#define ST_DE2 0        // 0: as deep as shared memory allows (below)
 #endif
 #ifndef ST_ROT2
 #define ST_ROT2 0
 #endif
   // producer-streamed boxes (wave): level 0 gets u^{n-1} and the medium of its plane (GH rows),
   // level 1 gets u^n and the medium of its plane (OY rows); DE entries per ring.
-  static constexpr int DE = ST_DE2;
   static constexpr int XSE = HX0 % 4;              // keep the field box start 16-B aligned
   static constexpr int EBW = GW + (XSE ? 4 : 0);   // field box width (floats)
   // field part first (padded to 128 B: TMA destinations are 128-B aligned), then the medium
   static constexpr int E0_FIELD = (EBW * GH * 4 + 127) / 128 * 128, E0_BYTES = E0_FIELD + 128 * GH * 4;
   static constexpr int E1_FIELD = (EBW * OY * 4 + 127) / 128 * 128, E1_BYTES = E1_FIELD + 128 * OY * 4;
+  // E-ring depth: as deep as the shared memory left after the level rings and a u^n ring of
+  // R + 3 slots allows (2..8); measured: deeper E rings hide the DRAM latency of the medium.
+  static constexpr int SMEM_MAX = 227 * 1024;
+  static constexpr int DE_FIT = (SMEM_MAX - 2048 - (TK - 1) * DL * LVL_BYTES - (R + 3) * SLOT_BYTES) /
+                                (E0_BYTES + E1_BYTES);
+  static constexpr int DE = ST_DE2 ? ST_DE2 : (DE_FIT < 2 ? 2 : DE_FIT > 8 ? 8 : DE_FIT);
   static constexpr int BAR_BYTES = 2048;   // full[64] | empty[64] | lfull | lempty | E0 f/e | E1 f/e
   static constexpr int EBAR_OFF = 1792;
   static constexpr int LRING_OFF = BAR_BYTES;
@@ -125,7 +131,7 @@ struct Geom2 {
   static constexpr int FIXED_BYTES = E1_OFF + (WAVE ? DE * E1_BYTES : 0);
   static_assert(1024 + 16 * (TK - 1) * DL <= EBAR_OFF && EBAR_OFF + 32 * DE <= BAR_BYTES, "barrier area");
   static_assert(TK >= 2 && (!WAVE || TK == 2), "time-tiled kernel: wave TK = 2, heat TK >= 2");
-  static_assert(OY % 2 == 0 && NCW + 1 <= 32, "warp budget");
+  static_assert(OY % 2 == 0 && NCW + NPROD <= 32, "warp budget");
   static_assert(OX > 0, "tile too small for this radius / depth");
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
   static_assert(FIXED_BYTES % 128 == 0, "TMA ring alignment");
@@ -396,13 +402,14 @@ sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
   }
   __syncthreads();
 
-  if (warp == NCW) {
+  if (warp >= NCW) {
     // ------------------------------------------------------------------ producer warp
-    // lane 0 streams the u^n ring, lane 1 (wave) the E rings: the two streams run ahead of their
-    // consumers independently (each bounded by its own ring depth).
+    // warp NCW streams the u^n ring, warp NCW+1 (wave) the E rings: separate warps, so the two
+    // streams run ahead of their consumers independently (a sleeping try_wait of one stream
+    // never holds the other back; each is bounded by its own ring depth).
     const int p_first = zb - TK * R, n_arr = (ze - zb) + 2 * TK * R;
     const int gx = tx0 - G::HX0, gy = ty0 - (TK - 1) * R;
-    if (lane == 0) {
+    if (warp == NCW && lane == 0) {
       asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&maps.u)) : "memory");
       const uint32_t ring = sbase + G::FIXED_BYTES;
       int slot = 0;
@@ -414,7 +421,7 @@ sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
                       p_first + a - p.zv_lo);
         if (++slot == nslot) { slot = 0; ph ^= 1u; }
       }
-    } else if (WAVE && lane == 1) {
+    } else if (WAVE && warp == NCW + 1 && lane == 0) {
       const uint32_t ebar = sbase + G::EBAR_OFF;
       int es = 0;
       uint32_t eph = 0;

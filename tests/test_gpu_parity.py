@@ -144,3 +144,15 @@ def test_run_to_run_determinism(name, tk, nt):
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
     assert np.abs(a[1]).max() > 0
+
+
+# ----------------------------------------------------------------------------- paper replica
+@pytest.mark.parametrize("tk", [1, 2])
+def test_paper_replica_scaled(tk):
+    """Source-free SO8 AWE with the paper's dt, h and Gaussian initial field (NEXT-2 i), ragged grid."""
+    _check(W.problem("P256", n=(70, 45, 38), nt=13, sponge=5), t_kernel=tk)
+
+
+@pytest.mark.parametrize("name,nt", [("P256", 8), ("P384", 4)])
+def test_paper_replica_full_grid(name, nt):
+    _check(W.problem(name), nt=nt, t_kernel=1)

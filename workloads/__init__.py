@@ -30,7 +30,13 @@ __all__ = [
     "velocity", "damp", "wavelet", "eigenmode_2d", "CONFIG_NAMES",
 ]
 
-CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")
+CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5", "P256", "P256L", "P384")
+
+# Paper-replica workloads (SURVEY.md §8(f) NEXT-2 i): the paper's own source-free AWE SO8 runs
+# (P:1787-1815): grid N^3 inside an (N+20)^3 array whose loops update indices
+# 4..N+15, dt = 3.04 and h = 20 (the printed constants, P:1678-1708 =
+# 2dt^2/h^2 x SO8 weights), Gaussian sigma = 0.4 on [-1, 1]^3 over the whole array.
+PAPER_REPLICA = {"P256": (256, 33), "P256L": (256, 247), "P384": (384, 165)}
 
 _GOLDEN = np.uint64(0x9E3779B97F4A7C15)
 _M1 = np.uint64(0xBF58476D1CE4E5B9)
@@ -63,7 +69,7 @@ class Problem:
     dt: float
     dx: Tuple[float, float, float]
     nt: int
-    init: str                      # "uniform" | "zero" | "eigenmode"
+    init: str                      # "uniform" | "zero" | "eigenmode" | "gaussian"
     seed: int = 0
     layers: Optional[Tuple[float, ...]] = None   # velocity per equal-thickness z-layer (m/s)
     perturb: float = 0.0           # relative velocity perturbation amplitude (C4: 0.05)
@@ -140,6 +146,12 @@ def problem(name: str, n: Optional[Sequence[int]] = None, nt: Optional[int] = No
                        nt if nt is not None else 2000, "zero", layers=layers, f_peak=15.0,
                        sponge=sp, src=(_centre(nn),),
                        rec=_receiver_lattice(nn, z=min(sp, nn[2] - 1), margin=sp))
+    if name in PAPER_REPLICA:
+        N, steps = PAPER_REPLICA[name]
+        nn = tuple(n) if n is not None else (N + 12, N + 12, N + 12)   # (N+20) - 2*4 updated
+        sp = 6 if sponge is None else sponge   # Devito's 10-point layer minus the 4-point halo
+        return Problem(name, 3, nn, 8, 2, 3.04, (20.0, 20.0, 20.0), nt if nt is not None else steps,
+                       "gaussian", layers=(1.5, 2.5), sponge=sp)
     raise ValueError(f"unknown config {name!r}")
 
 
@@ -161,6 +173,9 @@ def initial_fields(p: Problem, z0: int = 0, z1: Optional[int] = None):
     if p.init == "eigenmode":
         assert p.ndim == 2
         return u_prev, eigenmode_2d(nx, ny)[None].copy()
+    if p.init == "gaussian":
+        g = gaussian_3d(p.n, z0, z1)
+        return g.copy(), g
     u = np.zeros(shape, np.float32)
     plane = np.uint64(nx * ny)
     base = (np.arange(ny, dtype=np.uint64)[:, None] * np.uint64(nx)
@@ -169,6 +184,25 @@ def initial_fields(p: Problem, z0: int = 0, z1: Optional[int] = None):
         if 0 <= z < nz:
             u[k] = uniform01(p.seed, np.uint64(z) * plane + base)
     return u_prev, u
+
+
+def gaussian_3d(n, z0: int = 0, z1: Optional[int] = None, sigma: float = 0.4, halo: int = 4) -> np.ndarray:
+    """The paper's initial field: multivariate normal pdf, mean 0, sigma 0.4 per axis,
+    on np.mgrid[-1:1:A j] over the whole array of A = n + 2*halo points per axis; interior index i
+    sits at array index i + halo.  fp64, rounded to fp32.  Planes outside [0, nz) are 0."""
+    nx, ny, nz = n
+    z1 = nz if z1 is None else z1
+
+    def axis(m, idx):
+        a = m + 2 * halo
+        x = -1.0 + 2.0 * (np.asarray(idx, dtype=np.float64) + halo) / (a - 1)
+        return np.exp(-x * x / (2.0 * sigma * sigma))
+    gx = axis(nx, np.arange(nx))
+    gy = axis(ny, np.arange(ny))
+    zs = np.arange(z0, z1)
+    gz = np.where((zs >= 0) & (zs < nz), axis(nz, zs), 0.0)
+    norm = 1.0 / ((2.0 * np.pi) ** 1.5 * sigma ** 3)
+    return (norm * gz[:, None, None] * gy[None, :, None] * gx[None, None, :]).astype(np.float32)
 
 
 def eigenmode_2d(nx: int, ny: int, dtype=np.float32) -> np.ndarray:
