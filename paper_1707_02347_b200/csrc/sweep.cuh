@@ -39,6 +39,7 @@ struct SweepParams {
   float* outC;                // TK>1: u^{n+TK}
   const float4* ac;           // medium {a(x),a(x+1),c(x),c(x+1)} per column pair; row = X/2 float4
   int write_prev;             // TK>1 heat: also write u^{n+TK-1}
+  unsigned zero;              // always 0 (see zero_after)
   float K0, dt;
   float W[3][kMaxR + 1];      // W[axis][k]
   // sources (array-plane sorted): entries (x, y, plane, original index)
@@ -84,6 +85,15 @@ __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
 __device__ __forceinline__ float lo_of(uint64_t v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float hi_of(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
 __device__ __forceinline__ uint64_t splat(float w) { return pack2(w, w); }
+
+// 0, computed from v and the runtime zero p.zero (so neither nvcc nor ptxas can fold it): adding
+// it to an address makes the consumer of that address wait for v (e.g. an LDS result).
+__device__ __forceinline__ uint32_t zero_after(uint64_t v, uint32_t zero) {
+  uint32_t z;
+  asm volatile("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tand.b32 %0, lo, %2;\n\t}"
+               : "=r"(z) : "l"(v), "r"(zero));
+  return z;
+}
 
 __device__ __forceinline__ uint64_t lds64(const float* p) {
   return *reinterpret_cast<const uint64_t*>(p);

@@ -75,9 +75,7 @@ struct Geom1 {
 #ifndef ST_ROT1
 #define ST_ROT1 0
 #endif
-  // cp.async staging distance (planes).  VY = 2 uses 2: the (12 warps x 2 rows) geometry gave
-  // run-to-run different fields with distance 3 and 4 (unexplained), never with 2.
-  static constexpr int PD = ST_PD ? ST_PD : (VY == 1 ? 4 : 2);
+  static constexpr int PD = ST_PD ? ST_PD : 4;     // cp.async staging distance (planes)
   static constexpr int STAGE_F = VY * (64 + 128);  // staged plane rows: u^{n-1} (VY x 64) + {a,c} (VY x 128)
   static constexpr int STAGE_BYTES = NCW * (PD + 1) * STAGE_F * 4;
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
@@ -224,7 +222,15 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
         mbar_wait(&full[slot_a], ph_a);
 #pragma unroll
         for (int j = 0; j < VY; ++j) qn[u][j] = lds64(ring + slot_a * SLOT_F + col + j * BW);
-        if (idx < RZ) mbar_arrive(&empty[slot_a]);   // planes below zb are never a centre
+        if (idx < RZ) {
+          // planes below zb are never a centre: release the slot at once, but only after this
+          // lane's loads from it have returned (an LDS can sit behind the cp.async burst in the
+          // MIO queue long enough for the producer's next TMA into the slot to land first)
+          uint32_t z = 0;
+#pragma unroll
+          for (int j = 0; j < VY; ++j) z |= zero_after(qn[u][j], p.zero);
+          mbar_arrive(&empty[slot_a] + z);
+        }
         if (idx >= 2 * RZ) {                          // step s = s0 + idx in [zb, ze)
           if (WAVE) stage_next();                     // plane s + PD
           const int s = s0 + idx;

@@ -265,7 +265,8 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
       const uint32_t s = ring_in + in_slot * SLOT + my_in;
       q[iN][0] = ld_s64<0>(s);
       q[iN][1] = ld_s64<PB>(s);
-      if (a < R) mb_arrive(b_empty + 8 * in_slot);   // never a centre plane
+      // never a centre plane: release now, once this lane's loads from the slot have returned
+      if (a < R) mb_arrive(b_empty + 8 * in_slot + (zero_after(q[iN][0], p.zero) | zero_after(q[iN][1], p.zero)));
       if (++in_slot == nslot) { in_slot = 0; in_ph ^= 1u; }
     } else {
       mb_wait(lf_in + 8 * in_slot, in_ph);

@@ -20,7 +20,7 @@ if __name__ == "__main__":
         child(sys.argv[2], int(sys.argv[3]), int(sys.argv[4])); sys.exit(0)
     cfg, nt = sys.argv[1], sys.argv[2]
     libs = sys.argv[3].split(",") if len(sys.argv) > 3 else []
-    runs = [("main_tk2", None, 2)]
+    runs = [("main_tk2", None, 2), ("main_a", None, 1), ("main_b", None, 1), ("main_c", None, 1)]
     for v in libs:
         for rep in ("a", "b"):
             runs.append((f"{v}_{rep}", f"paper_1707_02347_b200/_varlib/libstencil_{v}.so", 1))
