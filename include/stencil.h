@@ -109,6 +109,20 @@ st_status stencil_run(stencil_plan *p, float *u_prev, float *u_cur, const float 
                       const int32_t *src_xyz, const float *src_wavelet, int32_t nrec,
                       const int32_t *rec_xyz, float *rec_trace);
 
+/* stencil_run plus snapshots of the full time dimension (the paper's "save" runs, where every
+ * time level is kept; SURVEY.md §8(f) NEXT-2 ii).  For j = 1 .. floor(nt/save_every)
+ * the field u^{n + j*save_every} is stored, in the field layout above, at
+ *   snapshots + (j-1)*snap_stride        (device fp32, caller-owned, snap_stride >= X*Y*Z floats).
+ * The store is fused into the sweep pass that produces that level (time-tiled passes are split so
+ * that none crosses a snapshot step); owned planes are written, ghost planes are not.
+ * Errors: as stencil_run, plus ST_EINVAL for save_every < 1, snapshots == NULL (when at least one
+ * snapshot is due) or snap_stride < X*Y*Z. */
+st_status stencil_run_save(stencil_plan *p, float *u_prev, float *u_cur, const float *vel,
+                           const float *damp, int32_t nt, int64_t step0, int32_t nsrc,
+                           const int32_t *src_xyz, const float *src_wavelet, int32_t nrec,
+                           const int32_t *rec_xyz, float *rec_trace, int32_t save_every,
+                           float *snapshots, int64_t snap_stride);
+
 /* Wait for the plan's stream; surfaces asynchronous CUDA errors (then ST_ECUDA, and the plan
  * enters ST_ESTATE). */
 st_status stencil_sync(stencil_plan *p);

@@ -17,9 +17,9 @@ STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 5: "S
                 6: "ST_ESTATE"}
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
-EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_sync", "stencil_destroy",
-           "stencil_last_error", "stencil_supported", "stencil_abi_version", "stencil_set_timing",
-           "stencil_timing")
+EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_run_save", "stencil_sync",
+           "stencil_destroy", "stencil_last_error", "stencil_supported", "stencil_abi_version",
+           "stencil_set_timing", "stencil_timing")
 
 
 class StConfig(ctypes.Structure):
@@ -68,6 +68,8 @@ def load():
     lib.stencil_run.argtypes = [P, P, P, P, P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, P, P,
                                 ctypes.c_int32, P, P]
     lib.stencil_run.restype = ctypes.c_int
+    lib.stencil_run_save.argtypes = lib.stencil_run.argtypes + [ctypes.c_int32, P, ctypes.c_int64]
+    lib.stencil_run_save.restype = ctypes.c_int
     lib.stencil_sync.argtypes = [P]
     lib.stencil_sync.restype = ctypes.c_int
     lib.stencil_destroy.argtypes = [P]

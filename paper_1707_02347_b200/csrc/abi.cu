@@ -222,7 +222,7 @@ struct Tables {
 
 extern "C" {
 
-int32_t stencil_abi_version(void) { return 100; }
+int32_t stencil_abi_version(void) { return 101; }
 
 int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel) {
   return st::find_kernel(ndim, time_order, radius, t_kernel) != nullptr ? 1 : 0;
@@ -450,10 +450,11 @@ static int choose_chunks(const stencil_plan* p, const st::KernelEntry* k, int bp
   return bestc;
 }
 
-st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
-                      const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
-                      const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
-                      const int32_t* rec_xyz, float* rec_trace) {
+static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
+                          const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
+                          const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
+                          const int32_t* rec_xyz, float* rec_trace, int32_t save_every,
+                          float* snapshots, int64_t snap_stride) {
   if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
   if (p->broken) return fail(p, ST_ESTATE, "plan is in an error state after an earlier CUDA fault");
   const st_config& c = p->cfg;
@@ -526,7 +527,9 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
   int launches = 0, tiled_launches = 0;
   if (p->timing) CK(cudaEventRecord(p->ev0, p->stream), "timing event");
   while (j < nt) {
-    const bool tiled = (c.t_kernel > 1) && (nt - j >= c.t_kernel);
+    // a time-tiled pass never crosses a snapshot step (passes end on multiples of save_every)
+    const bool tiled = (c.t_kernel > 1) && (nt - j >= c.t_kernel) &&
+                       (save_every <= 0 || (j % save_every) + c.t_kernel <= save_every);
     const int steps = tiled ? c.t_kernel : 1;
     const st::KernelEntry* k = tiled ? p->k_tk : p->k_t1;
     const int nslot = tiled ? p->nslot_tk : p->nslot_t1;
@@ -579,6 +582,9 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
       new_prev = op; new_cur = oc;
     }
     sp.write_prev = (j + steps == nt) ? 1 : 0;
+    sp.outS = (save_every > 0 && (j + steps) % save_every == 0)
+                  ? snapshots + (long long)((j + steps) / save_every - 1) * snap_stride
+                  : nullptr;
     sp.wl_step = step0 + j;
     sp.tr_step = j;
     const long long tiles = ((p->nx + k->ox - 1) / k->ox) * ((p->ny + k->oy - 1) / k->oy);
@@ -615,6 +621,29 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
   }
   if (p->timing) p->last_aux = aux_launches;
   return ST_OK;
+}
+
+st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
+                      const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
+                      const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
+                      const int32_t* rec_xyz, float* rec_trace) {
+  return run_impl(p, u_prev, u_cur, vel, damp, nt, step0, nsrc, src_xyz, src_wavelet, nrec, rec_xyz,
+                  rec_trace, 0, nullptr, 0);
+}
+
+st_status stencil_run_save(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
+                           const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
+                           const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
+                           const int32_t* rec_xyz, float* rec_trace, int32_t save_every,
+                           float* snapshots, int64_t snap_stride) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  if (save_every < 1) return fail(p, ST_EINVAL, "save_every must be >= 1 (got %d)", save_every);
+  if (!snapshots && nt >= save_every) return fail(p, ST_EINVAL, "snapshots is NULL");
+  if (snap_stride < p->X * p->Y * p->Z)
+    return fail(p, ST_EINVAL, "snap_stride (%lld) smaller than one field (%lld floats)",
+                (long long)snap_stride, (long long)(p->X * p->Y * p->Z));
+  return run_impl(p, u_prev, u_cur, vel, damp, nt, step0, nsrc, src_xyz, src_wavelet, nrec, rec_xyz,
+                  rec_trace, save_every, snapshots, snap_stride);
 }
 
 }  // extern "C"

@@ -37,6 +37,7 @@ struct SweepParams {
   const float* C;             // u^n (also read through the tensor map)
   float* outP;                // TK==1: u^{n+1} (may alias P); TK>1: u^{n+TK-1}
   float* outC;                // TK>1: u^{n+TK}
+  float* outS;                // snapshot of this pass's last level (same layout), or nullptr
   const float4* ac;           // medium {a(x),a(x+1),c(x),c(x+1)} per column pair; row = X/2 float4
   int write_prev;             // TK>1 heat: also write u^{n+TK-1}
   unsigned zero;              // always 0 (see zero_after)
@@ -421,6 +422,10 @@ sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ 
                 if (yin[j]) {
                   if (xin1) sts64(dst + j * p.X, out0[j]);
                   else dst[j * p.X] = lo_of(out0[j]);
+                  if (p.outS) {
+                    float* sn = p.outS + (long long)s * p.plane + rowoff + j * p.X;
+                    if (xin1) sts64(sn, out0[j]); else sn[0] = lo_of(out0[j]);
+                  }
                 }
               }
             }
@@ -492,9 +497,11 @@ sweep_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ 
                   if (xin1) {
                     sts64(p.outC + off + j * p.X, ol[j]);
                     if (WAVE || p.write_prev) sts64(p.outP + off + j * p.X, pv);
+                    if (p.outS) sts64(p.outS + off + j * p.X, ol[j]);
                   } else {
                     p.outC[off + j * p.X] = lo_of(ol[j]);
                     if (WAVE || p.write_prev) p.outP[off + j * p.X] = lo_of(pv);
+                    if (p.outS) p.outS[off + j * p.X] = lo_of(ol[j]);
                   }
                 }
               }

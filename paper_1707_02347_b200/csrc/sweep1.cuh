@@ -179,6 +179,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   const float* gP = p.P + (long long)zb * plane + (long long)y0 * X + x0;   // plane zb
   const float4* gA = p.ac + (long long)zb * (plane >> 1) + (long long)y0 * X2 + (x0 >> 1);
   float* out = p.outP + (long long)zb * plane + (long long)y0 * X + x0;
+  float* outs = p.outS ? p.outS + (long long)zb * plane + (long long)y0 * X + x0 : nullptr;   // snapshot
   int q_iss = zb;                                   // next plane to stage
   int e_use = 0, e_iss = 0;                         // staging entries of plane s and of q_iss
   auto stage_next = [&]() {                         // stage plane q_iss (if in the chunk)
@@ -264,6 +265,10 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
               if (yin[j]) {
                 if (xin1) sts64(out + j * X, o[j]);
                 else out[j * X] = lo_of(o[j]);
+                if (outs) {
+                  if (xin1) sts64(outs + j * X, o[j]);
+                  else outs[j * X] = lo_of(o[j]);
+                }
               }
             }
           }
@@ -275,6 +280,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
           mbar_arrive(&empty[slot_s]);
           if (++slot_s == nslot) slot_s = 0;
           out += plane;
+          if (outs) outs += plane;
         }
         if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
         if (ST_ROT1) {

@@ -317,6 +317,11 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
               if (yin0) { oc[0] = lo_of(o0); if (wr_prev) op[0] = lo_of(c0); }
               if (yin1) { oc[X] = lo_of(o1); if (wr_prev) op[X] = lo_of(c1); }
             }
+            if (p.outS) {   // snapshot of u^{n+TK}
+              float* os = p.outS + off;
+              if (xin1) { if (yin0) sts64(os, o0); if (yin1) sts64(os + X, o1); }
+              else { if (yin0) os[0] = lo_of(o0); if (yin1) os[X] = lo_of(o1); }
+            }
           }
         }
         if (wrec && qp >= zb && qp < ze && lane_out) {

@@ -100,9 +100,12 @@ class Stencil:
     def run(self, u_prev: torch.Tensor, u_cur: torch.Tensor, nt: int, vel: Optional[torch.Tensor] = None,
             damp: Optional[torch.Tensor] = None, step0: int = 0, src=None,
             wavelet: Optional[torch.Tensor] = None, rec=None,
-            trace: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+            trace: Optional[torch.Tensor] = None, save_every: int = 0,
+            snapshots: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
         """Advance (u_prev, u_cur) by nt steps in place (asynchronous on the plan's stream).
-        Returns the receiver trace tensor [nt, nrec] (allocated if not given)."""
+        Returns the receiver trace tensor [nt, nrec] (allocated if not given).
+        save_every > 0: also store u^{n + j*save_every}, j = 1..nt//save_every, into
+        snapshots[j-1] (a [nsnap, Z, Y, X] float32 CUDA tensor; stencil_run_save)."""
         for t in (u_prev, u_cur, vel, damp, wavelet, trace):
             if t is not None:
                 if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
@@ -115,12 +118,18 @@ class Stencil:
         if nrec and trace is None:
             trace = torch.zeros((nt, nrec), dtype=torch.float32, device=u_cur.device)
         lib = _lib.load()
-        st = lib.stencil_run(self._h, _ptr(u_prev), _ptr(u_cur), _ptr(vel), _ptr(damp), int(nt),
-                             int(step0), nsrc,
-                             None if src_a is None else src_a.ctypes.data_as(ctypes.c_void_p),
-                             _ptr(wavelet), nrec,
-                             None if rec_a is None else rec_a.ctypes.data_as(ctypes.c_void_p),
-                             _ptr(trace))
+        args = (self._h, _ptr(u_prev), _ptr(u_cur), _ptr(vel), _ptr(damp), int(nt), int(step0), nsrc,
+                None if src_a is None else src_a.ctypes.data_as(ctypes.c_void_p), _ptr(wavelet), nrec,
+                None if rec_a is None else rec_a.ctypes.data_as(ctypes.c_void_p), _ptr(trace))
+        if save_every:
+            if snapshots is None or not snapshots.is_cuda or snapshots.dtype != torch.float32 \
+                    or not snapshots.is_contiguous() or tuple(snapshots.shape[1:]) != self.shape \
+                    or snapshots.shape[0] < nt // save_every:
+                raise ValueError("snapshots must be a contiguous float32 CUDA tensor [nt//save_every, Z, Y, X]")
+            stride = self.shape[0] * self.shape[1] * self.shape[2]
+            st = lib.stencil_run_save(*args, int(save_every), _ptr(snapshots), stride)
+        else:
+            st = lib.stencil_run(*args)
         _lib.check(st, self._h)
         return trace
 

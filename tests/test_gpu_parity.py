@@ -156,3 +156,32 @@ def test_paper_replica_scaled(tk):
 @pytest.mark.parametrize("name,nt", [("P256", 8), ("P384", 4)])
 def test_paper_replica_full_grid(name, nt):
     _check(W.problem(name), nt=nt, t_kernel=1)
+
+
+# ----------------------------------------------------------------------------- snapshots (save mode)
+@pytest.mark.parametrize("tk,every", [(1, 3), (2, 3), (2, 4), (1, 1)])
+def test_snapshots_match_oracle(tk, every):
+    """stencil_run_save: snapshot j holds u^{j*every} bit-exactly (oracle run of j*every steps);
+    the run's final state is unchanged by saving (SURVEY §8(f) NEXT-2 ii)."""
+    import torch
+    from paper_1707_02347_b200 import Stencil
+    p = _wave("C3", (45, 38, 30), 10, 5, src=[(22, 19, 15)], rec=[(20, 20, 20)])
+    st = Stencil(p.ndim, p.n, p.space_order, p.time_order, p.dt, p.dx, t_kernel=tk)
+    up, uc = W.initial_fields(p)
+    P = st.embed(torch.from_numpy(up).cuda())
+    C = st.embed(torch.from_numpy(uc).cuda())
+    vel = st.embed(torch.from_numpy(W.velocity(p)).cuda())
+    damp = st.embed(torch.from_numpy(W.damp(p)).cuda())
+    wav = torch.from_numpy(W.wavelet(p, p.nt)).cuda()
+    nsnap = p.nt // every
+    snaps = torch.full((nsnap,) + st.shape, float("nan"), device="cuda")
+    st.run(P, C, p.nt, vel=vel, damp=damp, src=list(p.src), wavelet=wav, rec=list(p.rec),
+           save_every=every, snapshots=snaps)
+    st.sync()
+    for j in range(1, nsnap + 1):
+        _, want, _ = oracle_run(p, nt=j * every)
+        got = st.interior(snaps[j - 1]).cpu().numpy()
+        assert np.array_equal(got, want), j
+    _, want_c, _ = oracle_run(p)
+    assert np.array_equal(st.interior(C).cpu().numpy(), want_c)
+    st.close()
