@@ -32,8 +32,6 @@ import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
 
-# Best on-chip time-tile depth per config (measured)
-AUTO_TK = {"C1": 1, "C2": 1, "C3": 1, "C4": 1, "C5": 1, "P256": 1, "P256L": 1, "P384": 1}
 # The paper's own runs of the replica workloads (derived from P:2001-2003 and
 # P:2112-2116): GPts/s over the padded (N+20)^3 array, time-tiled and Devito auto-tuned blocking,
 # on a 4-core i7-6700K.  Context only (another machine, padded-point count).
@@ -138,9 +136,14 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     p = _problem(args.config, world)
-    tk = AUTO_TK[args.config] if args.tk == "auto" else int(args.tk)
-    tc = max(tk, args.tc) if world > 1 else tk
-    tc = tc if tc % tk == 0 else tk * ((tc + tk - 1) // tk)
+    from paper_1707_02347_b200.planner import plan
+    pl = plan(p.time_order, p.radius, p.n, nranks=world, ndim=p.ndim)
+    tk = pl.t_kernel if args.tk == "auto" else int(args.tk)
+    if world > 1:
+        tc = pl.t_comm if args.tc is None else max(tk, args.tc)
+        tc = tc if tc % tk == 0 else tk * ((tc + tk - 1) // tk)
+    else:
+        tc = tk
     nt = p.nt if args.nt is None else args.nt
     runner = SlabRunner(p, rank=rank, world=world, t_kernel=tk, t_comm=tc, device=local)
     st = runner.stencil
@@ -233,6 +236,7 @@ def run_gpu(args):
                 "workload": f"{args.config}: {_describe(p)}",
                 "grid": list(p.n), "nt_per_step": nt, "space_order": p.space_order,
                 "time_order": p.time_order, "t_kernel": tk, "t_comm": tc if world > 1 else None,
+                "schedule": pl.reason if args.tk == "auto" else f"t_kernel={tk} forced by --tk (planner: {pl.reason})",
                 "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (fields %.0f MiB each, L2 126 MB); no flush" % (
                     runner.field_bytes / 2**20),
@@ -364,7 +368,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=list(W.CONFIG_NAMES))
     ap.add_argument("--tk", default="auto")
-    ap.add_argument("--tc", type=int, default=4, help="halo depth in steps for N > 1")
+    ap.add_argument("--tc", type=int, default=None, help="halo depth in steps for N > 1 (default: planner)")
     ap.add_argument("--nt", type=int, default=None, help="override time steps per bench step")
     ap.add_argument("--so", type=int, default=None, help="override the space order (study runs only)")
     ap.add_argument("--grid", default=None, help="override the interior grid, e.g. 512x512x512 (study runs only)")
