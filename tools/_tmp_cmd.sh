@@ -1,4 +1,4 @@
-python tools/_cmp_runs.py C5 600 > gpurun_out/cmp.log 2>&1
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/fix_bench_C5.json 2>&1
-timeout 600 python bench.py --config C3 --tk 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/fix_bench_C3.json 2>&1
-timeout 600 python bench.py --config C4 --tk 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/fix_bench_C4.json 2>&1
+O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "ragged or tiny or composition or replica or snapshots or full_grid" > $O/m_pytest.log 2>&1; echo "exit $?" >> $O/m_pytest.log
+for c in C5 C3 C4; do timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/m_bench_$c.json 2>&1; done
+python tools/_cmp_runs.py C5 600 > $O/cmp.log 2>&1
