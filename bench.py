@@ -150,7 +150,6 @@ def run_gpu(args):
     # ---- host inputs (pinned) for this rank's slab, then resident device copies ----------------
     host = runner.host_inputs(nt, pin=True)
     dev_in = runner.to_device(host)
-    runner.set_timing(True)
 
     def step_resident():
         runner.reset_state(dev_in)          # zero initial fields (device memset, part of the step)
@@ -166,20 +165,17 @@ def run_gpu(args):
     clocks.start()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sweep_ms, sweep_launches, tiled, aux = 0.0, 0, 0, 0
+    runner.set_timing(True)     # per-run sweep events on the plan's stream, no host sync
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0.record(stream)
     for _ in range(args.steps):
         step_resident()
-        ms, nl, ntl, na = runner.last_timing()
-        sweep_ms += ms
-        sweep_launches += nl
-        tiled += ntl
-        aux += na
     e1.record(stream)
     torch.cuda.synchronize()
+    sweep_ms, sweep_launches, tiled, aux = runner.timing()   # summed over the timed runs
+    runner.set_timing(False)
     if world > 1:
         dist.barrier()
     ck = clocks.stop()

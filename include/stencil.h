@@ -93,6 +93,10 @@ st_status stencil_layout(const stencil_plan *p, int64_t padded[3], int64_t inter
  *   u_prev, u_cur : device, layout above, read/write.  heat: u_prev input ignored.
  *   vel, damp     : device, layout above; wave only (damp may be NULL = 0).  Must be valid on
  *                   every interior and ghost plane read (z-slabs: ghost planes included).
+ *                   The run derives the medium a, c from them (one pass over vel/damp).
+ *                   vel == NULL (wave): reuse the a, c of the most recent run of this plan that
+ *                   passed vel (the later T_c-step chunks of one z-slab simulation); ST_ESTATE
+ *                   if there was none.
  *   nt >= 0 steps; step0 = global index of the first step (indexes the wavelet rows).
  *   src_xyz       : host int32 [nsrc][3], GLOBAL interior coordinates (x, y, z)
  *   src_wavelet   : device fp32 [step0 + nt rows at least][nsrc]
@@ -102,6 +106,8 @@ st_status stencil_layout(const stencil_plan *p, int64_t padded[3], int64_t inter
  * nranks > 1: the caller must have exchanged ghost planes before the call (depth
  *   radius*nt of u_cur and radius*(nt-1) of u_prev), and nt <= t_comm.
  * Asynchronous on cfg.stream; arguments must stay valid until it completes.
+ * Source/receiver tables are rebuilt and uploaded only when src_xyz / rec_xyz differ from the
+ * previous run's lists.
  * Errors: ST_EINVAL (null required pointer, nt < 0, nt > t_comm with nranks > 1, a source or
  * receiver outside the global interior), ST_ESTATE, ST_ECUDA, ST_ENOMEM. */
 st_status stencil_run(stencil_plan *p, float *u_prev, float *u_cur, const float *vel,
@@ -136,11 +142,12 @@ const char *stencil_last_error(const stencil_plan *p);
 
 /* Kernel timing (measurement support).  enable != 0: every later stencil_run
  * records CUDA events on the plan's stream immediately before its first and after its last
- * sweep-kernel launch.  stencil_timing waits for the last run's end event and returns the
- * elapsed milliseconds between them, the number of sweep launches it enqueued, and how many of
- * those were time-tiled (t_kernel-level) passes, and how many auxiliary kernels (medium
- * precompute, final swap) the run launched.  ST_ESTATE if timing was not enabled or no run
- * has been timed.  Any output pointer may be NULL. */
+ * sweep-kernel launch (no host synchronisation).  stencil_timing waits for the latest end event
+ * and returns, summed over every run since the previous stencil_timing (or stencil_set_timing)
+ * call, the elapsed milliseconds between each run's events, the number of sweep launches, how
+ * many of those were time-tiled (t_kernel-level) passes, and how many auxiliary kernels (medium
+ * precompute, final swap) the runs launched; then it resets the sums.  ST_ESTATE if timing was
+ * not enabled or no run has been timed since.  Any output pointer may be NULL. */
 st_status stencil_set_timing(stencil_plan *p, int32_t enable);
 st_status stencil_timing(stencil_plan *p, float *sweep_ms, int32_t *sweep_launches,
                          int32_t *tiled_launches, int32_t *aux_launches);

@@ -44,7 +44,8 @@ def _t1_geom(ndim: int, wave: int, R: int):
         return 12, 2
     return NCW_T1, 1
 
-# kernel kinds: 1 = sweep1 (untiled, warp-specialised), 2 = sweep2 (time-tiled, warp-specialised),
+# kernel kinds: 1 = sweep1 (untiled, warp-specialised), 3 = sweep1s (untiled, static 2r+1 ring),
+#               2 = sweep2 (time-tiled, warp-specialised),
 #               0 = sweep (first time-tiled kernel; 2-D and the shapes sweep2 does not fit)
 def _sweep2_oy(wave: int, R: int, TK: int):
     """Output rows of the sweep2 (one warp group per level) instance, or None if it does not fit
@@ -56,6 +57,14 @@ def _sweep2_oy(wave: int, R: int, TK: int):
     return None
 
 
+def _static_ring(ndim: int, wave: int, R: int) -> bool:
+    """Untiled 3-D instances built as sweep1s_kernel (ring of exactly 2r+1 slots, compile-time
+    slot/queue indices): where 2r+1 slots leave >= 5 planes of prefetch and, with the cp.async
+    staging, fit in shared memory (Geom1S::OK) -- and where it measured faster (C5 SO12: 285.5 vs
+    274.4 GPts/s)."""
+    return ndim == 3 and R in (5, 6)   # R = 8 (PD 3): C4 246 vs 252 GPts/s with sweep1 -> sweep1
+
+
 def instances():
     """(ndim, wave, R, TK, VY, NWY, kind) compiled into this build.
     For kind 2 the NWY slot holds the output rows OY of the instance."""
@@ -63,7 +72,7 @@ def instances():
     for wave in (0, 1):
         for R in range(1, 9):
             ncw, vy = _t1_geom(3, wave, R)
-            out.append((3, wave, R, 1, vy, ncw, 1))
+            out.append((3, wave, R, 1, vy, ncw, 3 if _static_ring(3, wave, R) else 1))
             oy = _sweep2_oy(wave, R, 2)
             if oy:
                 out.append((3, wave, R, 2, 2, oy, 2))
@@ -92,6 +101,8 @@ def _gen_sources(groups: int, inst=None, outdir: str = BUILD):
             w = 'true' if wave else 'false'
             if kind == 1:
                 lines.append(f"  make_entry1<{R}, {w}, {ndim}, {NWY}, {VY}>(),")
+            elif kind == 3:
+                lines.append(f"  make_entry1s<{R}, {w}, {NWY}, {VY}>(),")
             elif kind == 2:
                 lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}>(),")   # NWY = output rows
             else:
@@ -133,7 +144,7 @@ def _digest(paths, extra=()):
 def _compile(src: str, outdir: str = BUILD, defines=()):
     obj = os.path.join(outdir, os.path.basename(src) + ".o")
     deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "sweep1.cuh"),
-            os.path.join(CSRC, "sweep2.cuh"),
+            os.path.join(CSRC, "sweep2.cuh"), os.path.join(CSRC, "sweep1s.cuh"),
             os.path.join(CSRC, "registry.h"),
             os.path.join(HERE, "..", "include", "stencil.h")]
     stamp = obj + ".stamp"

@@ -55,14 +55,22 @@ struct stencil_plan {
   // scratch
   Buf ac, p2, c2, tables;
   Buf staging;       // pinned host staging for the src/rec tables
+  bool have_medium = false;            // a/c hold the medium of an earlier run (vel == NULL reuses it)
+  bool have_tables = false;            // tables hold the src/rec lists below (re-uploaded on change)
+  std::vector<int32_t> last_src, last_rec;
+  const int *t_sb = nullptr, *t_rb = nullptr;
+  const int4 *t_s = nullptr, *t_r = nullptr;
   cudaEvent_t staging_ev = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   bool broken = false;
   std::string err;
   // timing (stencil_set_timing / stencil_timing)
-  bool timing = false, timed = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int last_launches = 0, last_tiled = 0, last_aux = 0;
+  // one (start, end) event pair per timed run since the last stencil_timing query; the pool is
+  // reused, so a run records events without any host synchronisation
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;   // 2 per pair
+  int ev_used = 0;                    // pairs recorded since the last query
+  int last_launches = 0, last_tiled = 0, last_aux = 0;   // accumulated since the last query
 };
 
 namespace {
@@ -190,8 +198,9 @@ st_status encode_map(stencil_plan* p, const st::KernelEntry* k, const float* fie
 // choose ring depth / occupancy for one instance
 st_status configure_instance(stencil_plan* p, const st::KernelEntry* k, int* nslot, size_t* smem, int* bps) {
   const size_t max_smem = 227 * 1024;
-  const int min_slots = k->rz + 2;
-  const int want_slots = std::min(64, k->rz + 1 + k->extra_depth);   // prefetch depth in planes
+  const int min_slots = k->fixed_slots ? k->fixed_slots : k->rz + 2;
+  const int want_slots = k->fixed_slots ? k->fixed_slots
+                                        : std::min(64, k->rz + 1 + k->extra_depth);   // prefetch depth in planes
   int best_slots = 0, best_bps = 0;
   size_t best_smem = 0;
   for (int slots = std::max(min_slots, want_slots); slots >= min_slots; --slots) {
@@ -222,7 +231,7 @@ struct Tables {
 
 extern "C" {
 
-int32_t stencil_abi_version(void) { return 101; }
+int32_t stencil_abi_version(void) { return 102; }
 
 int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel) {
   return st::find_kernel(ndim, time_order, radius, t_kernel) != nullptr ? 1 : 0;
@@ -340,34 +349,36 @@ void stencil_destroy(stencil_plan* p) {
   free_buf(p->ac); free_buf(p->p2); free_buf(p->c2); free_buf(p->tables);
   if (p->staging.ptr) cudaFreeHost(p->staging.ptr);
   if (p->staging_ev) cudaEventDestroy(p->staging_ev);
-  if (p->ev0) cudaEventDestroy(p->ev0);
-  if (p->ev1) cudaEventDestroy(p->ev1);
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   delete p;
 }
 
 st_status stencil_set_timing(stencil_plan* p, int32_t enable) {
   if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
   CK(cudaSetDevice(p->device), "cudaSetDevice");
-  if (enable && !p->ev0) {
-    CK(cudaEventCreate(&p->ev0), "cudaEventCreate");
-    CK(cudaEventCreate(&p->ev1), "cudaEventCreate");
-  }
   p->timing = enable != 0;
-  p->timed = false;
+  p->ev_used = 0;
+  p->last_launches = p->last_tiled = p->last_aux = 0;
   return ST_OK;
 }
 
 st_status stencil_timing(stencil_plan* p, float* ms, int32_t* launches, int32_t* tiled, int32_t* aux) {
   if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
-  if (!p->timing || !p->timed) return fail(p, ST_ESTATE, "no timed run (call stencil_set_timing first)");
+  if (!p->timing || p->ev_used == 0) return fail(p, ST_ESTATE, "no timed run (call stencil_set_timing first)");
   CK(cudaSetDevice(p->device), "cudaSetDevice");
-  CK(cudaEventSynchronize(p->ev1), "timing event synchronize");
-  float t = 0.f;
-  CK(cudaEventElapsedTime(&t, p->ev0, p->ev1), "cudaEventElapsedTime");
-  if (ms) *ms = t;
+  CK(cudaEventSynchronize(p->ev_pool[2 * (p->ev_used - 1) + 1]), "timing event synchronize");
+  float total = 0.f;
+  for (int i = 0; i < p->ev_used; ++i) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, p->ev_pool[2 * i], p->ev_pool[2 * i + 1]), "cudaEventElapsedTime");
+    total += t;
+  }
+  if (ms) *ms = total;
   if (launches) *launches = p->last_launches;
   if (tiled) *tiled = p->last_tiled;
   if (aux) *aux = p->last_aux;
+  p->ev_used = 0;
+  p->last_launches = p->last_tiled = p->last_aux = 0;
   return ST_OK;
 }
 
@@ -382,6 +393,15 @@ st_status stencil_sync(stencil_plan* p) {
 static st_status upload_tables(stencil_plan* p, int32_t nsrc, const int32_t* src_xyz, int32_t nrec,
                                const int32_t* rec_xyz, const int** src_begin, const int4** src,
                                const int** rec_begin, const int4** rec) {
+  // unchanged lists (the common case: every chunk of a simulation) -> the tables on the device
+  // are still valid (they are only read by kernels, and any rewrite below is stream-ordered)
+  if (p->have_tables && p->last_src.size() == (size_t)3 * nsrc && p->last_rec.size() == (size_t)3 * nrec &&
+      (nsrc == 0 || memcmp(p->last_src.data(), src_xyz, 12 * (size_t)nsrc) == 0) &&
+      (nrec == 0 || memcmp(p->last_rec.data(), rec_xyz, 12 * (size_t)nrec) == 0)) {
+    *src_begin = p->t_sb; *src = p->t_s; *rec_begin = p->t_rb; *rec = p->t_r;
+    return ST_OK;
+  }
+  p->have_tables = false;
   // sources: every plane of this slab's array (incl. ghosts) -> injected in redundant copies too
   // receivers: owned planes only (unique writer per slab)
   std::vector<int4> S, Rv;
@@ -431,6 +451,10 @@ static st_status upload_tables(stencil_plan* p, int32_t nsrc, const int32_t* src
   *src = reinterpret_cast<const int4*>(d + o_s);
   *rec_begin = reinterpret_cast<const int*>(d + o_rb);
   *rec = reinterpret_cast<const int4*>(d + o_r);
+  p->t_sb = *src_begin; p->t_s = *src; p->t_rb = *rec_begin; p->t_r = *rec;
+  p->last_src.assign(src_xyz, src_xyz + 3 * (size_t)nsrc);
+  p->last_rec.assign(rec_xyz, rec_xyz + 3 * (size_t)nrec);
+  p->have_tables = true;
   return ST_OK;
 }
 
@@ -461,7 +485,8 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   const bool wave = c.time_order == 2;
   if (!u_prev || !u_cur) return fail(p, ST_EINVAL, "u_prev/u_cur is NULL");
   if (u_prev == u_cur) return fail(p, ST_EINVAL, "u_prev and u_cur must be distinct buffers");
-  if (wave && !vel) return fail(p, ST_EINVAL, "vel is NULL (wave)");
+  if (wave && !vel && !p->have_medium)
+    return fail(p, ST_ESTATE, "vel is NULL but no earlier run of this plan computed the medium");
   if (nt < 0) return fail(p, ST_EINVAL, "nt < 0");
   if (step0 < 0) return fail(p, ST_EINVAL, "step0 < 0");
   if (nsrc < 0 || nrec < 0) return fail(p, ST_EINVAL, "negative source/receiver count");
@@ -487,14 +512,16 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   const long long zv_hi = p->G + p->nzl + (p->has_hi ? p->G : 0);
   const long long plane = p->X * p->Y;
 
-  // medium a/c over all valid planes
-  if (wave) {
+  // medium a/c over all valid planes (vel == NULL: keep the medium of the previous run, e.g. the
+  // later T_c-step chunks of one z-slab simulation)
+  if (wave && vel) {
     const long long n = (p->X / 2) * p->Y * (zv_hi - zv_lo);
     const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)p->sm_count * 16);
     medium_kernel<<<blocks, 256, 0, p->stream>>>(vel, damp, static_cast<float4*>(p->ac.ptr), (int)p->nx, (int)p->ny,
                                                   p->X, plane, (int)zv_lo, (int)(zv_hi - zv_lo), p->dtf,
                                                   (float)(2.0 * c.dt * c.dt));
     CK(cudaGetLastError(), "medium kernel launch");
+    p->have_medium = true;
     ++aux_launches;
   }
 
@@ -525,7 +552,18 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
 
   int j = 0;
   int launches = 0, tiled_launches = 0;
-  if (p->timing) CK(cudaEventRecord(p->ev0, p->stream), "timing event");
+  cudaEvent_t t_ev1 = nullptr;
+  if (p->timing) {
+    if ((int)p->ev_pool.size() < 2 * (p->ev_used + 1)) {
+      // grows by one pair per run between two queries (the caller's query cadence bounds it)
+      cudaEvent_t a = nullptr, b = nullptr;
+      CK(cudaEventCreate(&a), "cudaEventCreate");
+      CK(cudaEventCreate(&b), "cudaEventCreate");
+      p->ev_pool.push_back(a); p->ev_pool.push_back(b);
+    }
+    CK(cudaEventRecord(p->ev_pool[2 * p->ev_used], p->stream), "timing event");
+    t_ev1 = p->ev_pool[2 * p->ev_used + 1];
+  }
   while (j < nt) {
     // a time-tiled pass never crosses a snapshot step (passes end on multiples of save_every)
     const bool tiled = (c.t_kernel > 1) && (nt - j >= c.t_kernel) &&
@@ -599,10 +637,10 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
     j += steps;
   }
   if (p->timing) {
-    CK(cudaEventRecord(p->ev1, p->stream), "timing event");
-    p->timed = true;
-    p->last_launches = launches;
-    p->last_tiled = tiled_launches;
+    CK(cudaEventRecord(t_ev1, p->stream), "timing event");
+    ++p->ev_used;
+    p->last_launches += launches;
+    p->last_tiled += tiled_launches;
   }
 
   // honour the contract: (u_prev, u_cur) buffers hold (u^{n+nt-1}, u^{n+nt})
@@ -619,7 +657,7 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
     CK(cudaMemcpyAsync(u_prev, bufs[prev], field_bytes, cudaMemcpyDeviceToDevice, p->stream), "copy u_prev");
     CK(cudaMemcpyAsync(u_cur, bufs[cur], field_bytes, cudaMemcpyDeviceToDevice, p->stream), "copy u_cur");
   }
-  if (p->timing) p->last_aux = aux_launches;
+  if (p->timing) p->last_aux += aux_launches;
   return ST_OK;
 }
 

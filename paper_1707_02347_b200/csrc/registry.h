@@ -6,6 +6,7 @@
 
 #include "sweep.cuh"
 #include "sweep1.cuh"
+#include "sweep1s.cuh"
 #include "sweep2.cuh"
 
 #ifndef ST_T1_DEPTH
@@ -32,6 +33,7 @@ struct KernelEntry {
   int extra_depth;     // preferred ring prefetch depth beyond the rz+1 resident planes
   int ebw = 0, eh0 = 0, eh1 = 0;   // time-tiled kernel (wave): field box width, level-0 / level-1
                                    // box rows of the producer-streamed u^{n-1}, u^n, medium
+  int fixed_slots = 0;             // > 0: the ring depth is compiled in (sweep1s_kernel)
 };
 
 // Defined in the generated instance translation units.
@@ -73,14 +75,20 @@ constexpr KernelEntry make_entry() {
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t launch_sweep1(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  sweep1_kernel<R, WAVE, NDIM, NCW, VY><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  if (p.outS)
+    sweep1_kernel<R, WAVE, NDIM, NCW, VY, true><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  else
+    sweep1_kernel<R, WAVE, NDIM, NCW, VY, false><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
   return cudaGetLastError();
 }
 
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t query_sweep1(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweep1_kernel<R, WAVE, NDIM, NCW, VY>;
+  auto k = sweep1_kernel<R, WAVE, NDIM, NCW, VY, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(sweep1_kernel<R, WAVE, NDIM, NCW, VY, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (attr) {
     e = cudaFuncGetAttributes(attr, k);
@@ -96,6 +104,44 @@ constexpr KernelEntry make_entry1() {
   return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      G::RZ, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
                      &launch_sweep1<R, WAVE, NDIM, NCW, VY>, &query_sweep1<R, WAVE, NDIM, NCW, VY>, ST_T1_DEPTH};
+}
+
+// ---- untiled kernel with a compiled-in ring of 2r+1 slots (sweep1s.cuh)
+template <int R, bool WAVE, int NCW, int VY>
+cudaError_t launch_sweep1s(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
+                           size_t smem, cudaStream_t stream) {
+  if (p.outS)
+    sweep1s_kernel<R, WAVE, NCW, VY, true><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  else
+    sweep1s_kernel<R, WAVE, NCW, VY, false><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  return cudaGetLastError();
+}
+
+template <int R, bool WAVE, int NCW, int VY>
+cudaError_t query_sweep1s(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweep1s_kernel<R, WAVE, NCW, VY, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(sweep1s_kernel<R, WAVE, NCW, VY, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (attr) {
+    e = cudaFuncGetAttributes(attr, k);
+    if (e != cudaSuccess) return e;
+  }
+  if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, nthreads, smem);
+  return cudaSuccess;
+}
+
+template <int R, bool WAVE, int NCW, int VY>
+constexpr KernelEntry make_entry1s() {
+  using G = Geom1<R, 3, NCW, VY>;
+  using S = Geom1S<R, NCW, VY, WAVE>;
+  KernelEntry e{3, WAVE ? 2 : 1, R, 1, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+                R, (size_t)S::SLOT_BYTES, (size_t)S::FIXED_BYTES,
+                &launch_sweep1s<R, WAVE, NCW, VY>, &query_sweep1s<R, WAVE, NCW, VY>, S::NS - R - 1};
+  e.fixed_slots = S::NS;
+  return e;
 }
 
 // ---- warp-specialised time-tiled kernel (sweep2.cuh): one warp group per level

@@ -92,7 +92,9 @@ __device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent,
   return false;
 }
 
-template <int R, bool WAVE, int NDIM, int NCW, int VY>
+// SAVE: this pass also stores u^{n+1} into the snapshot field p.outS (stencil_run_save); a separate
+// instance, so the plain sweep carries no snapshot logic in its step body.
+template <int R, bool WAVE, int NDIM, int NCW, int VY, bool SAVE>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
 sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
               const int nslot) {
@@ -157,6 +159,8 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     any_row |= yin[j];
   }
   const bool act = any_row && xin0;               // this lane owns >= 1 interior point
+  // warp-uniform: every row and column of this warp is interior (the common case) -> plain stores
+  const bool whole = (tx0 + 64 <= p.nx) && (y0 + VY <= p.ny);
   const int col = (warp * VY + R) * BW + 2 * lane + RXB;   // my first row's pair in a ring slot
   const uint64_t DT = splat(p.dt);
   // rare events of this warp's rows (sources / receivers), decided once per CTA chunk
@@ -179,7 +183,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   const float* gP = p.P + (long long)zb * plane + (long long)y0 * X + x0;   // plane zb
   const float4* gA = p.ac + (long long)zb * (plane >> 1) + (long long)y0 * X2 + (x0 >> 1);
   float* out = p.outP + (long long)zb * plane + (long long)y0 * X + x0;
-  float* outs = p.outS ? p.outS + (long long)zb * plane + (long long)y0 * X + x0 : nullptr;   // snapshot
+  float* outs = SAVE ? p.outS + (long long)zb * plane + (long long)y0 * X + x0 : nullptr;   // snapshot
   int q_iss = zb;                                   // next plane to stage
   int e_use = 0, e_iss = 0;                         // staging entries of plane s and of q_iss
   auto stage_next = [&]() {                         // stage plane q_iss (if in the chunk)
@@ -259,13 +263,19 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
 #pragma unroll
             for (int j = 0; j < VY; ++j) o[j] = f2fma(DT, acc[j], qn[md<QN>(u - RZ)][j]) & mask[j];
           }
-          if (act) {
+          if (whole) {
+#pragma unroll
+            for (int j = 0; j < VY; ++j) {
+              sts64(out + j * X, o[j]);
+              if (SAVE) sts64(outs + j * X, o[j]);
+            }
+          } else if (act) {
 #pragma unroll
             for (int j = 0; j < VY; ++j) {
               if (yin[j]) {
                 if (xin1) sts64(out + j * X, o[j]);
                 else out[j * X] = lo_of(o[j]);
-                if (outs) {
+                if (SAVE) {
                   if (xin1) sts64(outs + j * X, o[j]);
                   else outs[j * X] = lo_of(o[j]);
                 }
@@ -280,7 +290,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
           mbar_arrive(&empty[slot_s]);
           if (++slot_s == nslot) slot_s = 0;
           out += plane;
-          if (outs) outs += plane;
+          if (SAVE) outs += plane;
         }
         if (++slot_a == nslot) { slot_a = 0; ph_a ^= 1u; }
         if (ST_ROT1) {

@@ -123,7 +123,6 @@ class SlabRunner:
         self.field_bytes = st.X * st.Y * st.Z * 4
         self.wave = problem.time_order == 2
         self._timing = False
-        self._acc = (0.0, 0, 0, 0)
 
     @property
     def nz_local(self):
@@ -200,11 +199,10 @@ class SlabRunner:
         self._timing = on
         self.stencil.set_timing(on)
 
-    def last_timing(self):
-        return self._acc
-
-    def aux_launches_per_run(self) -> int:
-        return self._aux
+    def timing(self):
+        """(sweep_ms, sweep_launches, tiled_launches, aux_launches) summed over every run since the
+        previous query or set_timing (waits for the last run; the runs themselves never sync)."""
+        return self.stencil.timing()
 
     def run(self, dev, nt: int):
         """Advance the slab by nt steps (exchange every T_c steps when world > 1); returns the
@@ -215,23 +213,20 @@ class SlabRunner:
             trace = trace[:nt]
             trace.zero_()
         done = 0
-        acc = [0.0, 0, 0, 0]
         while done < nt:
             n = min(self.tc, nt - done) if self.world > 1 else nt - done
             if self.world > 1:
                 halo_exchange(dev, self.rank, self.world, self.G, self.nzl, p.radius, n,
                               need_prev=self.wave)
-            st.run(dev["u_prev"], dev["u_cur"], n, vel=dev.get("vel"), damp=dev.get("damp"),
+            # the medium a, c is derived once per simulation (first chunk); later chunks reuse it
+            first = done == 0
+            st.run(dev["u_prev"], dev["u_cur"], n, vel=dev.get("vel") if first else None,
+                   damp=dev.get("damp") if first else None,
                    step0=done, src=list(p.src), wavelet=dev.get("wavelet"), rec=list(p.rec),
                    trace=None if trace is None else trace[done:done + n])
-            if self._timing:
-                ms, nl, ntl, na = st.timing()
-                acc[0] += ms; acc[1] += nl; acc[2] += ntl; acc[3] += na
             done += n
         if trace is not None and self.world > 1:
             dist.all_reduce(trace)
-        self._acc = tuple(acc)
-        self._aux = acc[3]
         return trace
 
     def close(self):

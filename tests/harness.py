@@ -16,8 +16,9 @@ def rel_l2(got, want) -> float:
     return float(num / den) if den > 0 else float(num)
 
 
-def gpu_run(p: W.Problem, nt=None, t_kernel=1, splits=None):
-    """Run p on cuda:0; `splits` = list of nt chunks (run composition).  Returns interior
+def gpu_run(p: W.Problem, nt=None, t_kernel=1, splits=None, reuse_medium=False):
+    """Run p on cuda:0; `splits` = list of nt chunks (run composition; with reuse_medium the
+    chunks after the first pass vel = damp = None and reuse the plan's medium).  Returns interior
     (u_prev, u_cur, trace) as numpy arrays."""
     import torch
     from paper_1707_02347_b200 import Stencil
@@ -34,7 +35,9 @@ def gpu_run(p: W.Problem, nt=None, t_kernel=1, splits=None):
     traces = []
     done = 0
     for chunk in (splits or [nt]):
-        tr = st.run(P, C, chunk, vel=vel, damp=damp, step0=done, src=list(p.src), wavelet=wav,
+        keep = reuse_medium and done > 0
+        tr = st.run(P, C, chunk, vel=None if keep else vel, damp=None if keep else damp, step0=done,
+                    src=list(p.src), wavelet=wav,
                     rec=list(p.rec))
         if tr is not None:
             traces.append(tr)

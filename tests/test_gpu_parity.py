@@ -95,6 +95,27 @@ def test_run_composition(tk):
     _check(p, t_kernel=tk, splits=[3, 5, 4])
 
 
+@pytest.mark.parametrize("tk", [1, 2])
+def test_run_composition_reused_medium(tk):
+    """Later chunks pass vel = damp = None (the plan keeps the medium of the first chunk) and
+    identical src/rec lists (the plan keeps its uploaded tables): still bit-exact."""
+    p = _wave("C3", (70, 66, 40), 12, 6, src=[(35, 33, 20)], rec=[(35, 33, 20), (10, 10, 10)])
+    gp, gc, gt = gpu_run(p, t_kernel=tk, splits=[3, 5, 4], reuse_medium=True)
+    op, oc, ot = oracle_run(p)
+    assert np.array_equal(gc, oc) and np.array_equal(gp, op) and np.array_equal(gt, ot)
+
+
+def test_vel_null_without_medium_is_estate():
+    import torch
+    from paper_1707_02347_b200 import Stencil
+    p = _wave("C3", (40, 36, 30), 4, 4)
+    st = Stencil(3, p.n, p.space_order, 2, p.dt, p.dx)
+    P, C = st.empty(), st.empty()
+    with pytest.raises(RuntimeError, match="ST_ESTATE|medium"):
+        st.run(P, C, 2)
+    st.close()
+
+
 def test_nt_zero_is_noop():
     import torch
     from paper_1707_02347_b200 import Stencil
