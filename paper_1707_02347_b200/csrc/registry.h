@@ -148,14 +148,20 @@ constexpr KernelEntry make_entry1s() {
 template <int R, int TK, bool WAVE, int OY>
 cudaError_t launch_sweep2(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  sweep2_kernel<R, TK, WAVE, OY><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(maps, p, nslot);
+  if (p.outS)
+    sweep2_kernel<R, TK, WAVE, OY, true><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(maps, p, nslot);
+  else
+    sweep2_kernel<R, TK, WAVE, OY, false><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(maps, p, nslot);
   return cudaGetLastError();
 }
 
 template <int R, int TK, bool WAVE, int OY>
 cudaError_t query_sweep2(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweep2_kernel<R, TK, WAVE, OY>;
+  auto k = sweep2_kernel<R, TK, WAVE, OY, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(sweep2_kernel<R, TK, WAVE, OY, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (attr) {
     e = cudaFuncGetAttributes(attr, k);

@@ -54,13 +54,30 @@ __device__ __forceinline__ void mb_arrive(uint32_t a) {
 __device__ __forceinline__ void mb_expect_tx(uint32_t a, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(bytes) : "memory");
 }
+// ST_WAIT2 (experiment): 0 = try_wait with a suspend-time hint (default), 1 = try_wait without
+// a hint, 2 = test_wait spin
+#ifndef ST_WAIT2
+#define ST_WAIT2 0
+#endif
 __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
   uint32_t ok = 0;
   do {
+#if ST_WAIT2 == 2
+    asm volatile("{\n\t.reg .pred q;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, q;\n\t}"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+#elif ST_WAIT2 == 1
+    asm volatile("{\n\t.reg .pred q;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, q;\n\t}"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+#else
     asm volatile("{\n\t.reg .pred q;\n\t"
                  "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 0x989680;\n\t"
                  "selp.u32 %0, 1, 0, q;\n\t}"
                  : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+#endif
   } while (!ok);
 }
 __device__ __forceinline__ void tma_load_3d_s(uint32_t dst, const CUtensorMap* map, uint32_t bar,
@@ -177,7 +194,7 @@ __device__ __forceinline__ void accum2(uint64_t (&acc)[2], const uint64_t (&q)[2
 }
 
 // One consumer warp of level L (group L): the whole z stream of the CTA's chunk.
-template <int L, int R, int TK, bool WAVE, int OY>
+template <int L, int R, int TK, bool WAVE, int OY, bool SAVE>
 __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot, const uint32_t sbase,
                                            const int warp, const int lane, const int tx0,
                                            const int ty0, const int zb, const int ze) {
@@ -200,6 +217,8 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
   const uint64_t m0 = yin0 ? xmask : 0ull, m1 = yin1 ? xmask : 0ull;
   const bool lane_out = (lane >= HX0 / 2) && (lane < 32 - HX0 / 2);   // output-tile lanes
   const bool row0_out = r0 >= HY0 && r0 < GH - HY0, row1_out = r0 + 1 >= HY0 && r0 + 1 < GH - HY0;
+  // last level: the warp's output columns [tx0, tx0 + OX) and both rows are interior
+  const bool whole = (tx0 + G::OX <= p.nx) && yin0 && yin1;
   const int p_first = zb - TK * R;
   const int n_arr = (ze - zb) + 2 * TK * R;
   // level L at step a computes plane p_first + a - (L+1)R; active on [a_lo, a_hi)
@@ -306,7 +325,14 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
         if (L == TK - 1) {
           // u^{n+TK} and u^{n+TK-1} on the output tile (every row of the last group is an
           // output row; the active range is exactly the output planes)
-          if (lane_out && xin0) {
+          if (whole) {                 // warp-uniform: both rows and all columns interior
+            if (lane_out) {
+              const long long off = obase + (long long)a * plane;
+              sts64(p.outC + off, o0); sts64(p.outC + off + X, o1);
+              if (wr_prev) { sts64(p.outP + off, c0); sts64(p.outP + off + X, c1); }
+              if (SAVE) { sts64(p.outS + off, o0); sts64(p.outS + off + X, o1); }
+            }
+          } else if (lane_out && xin0) {
             const long long off = obase + (long long)a * plane;
             float* oc = p.outC + off;
             float* op = p.outP + off;
@@ -317,7 +343,7 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
               if (yin0) { oc[0] = lo_of(o0); if (wr_prev) op[0] = lo_of(c0); }
               if (yin1) { oc[X] = lo_of(o1); if (wr_prev) op[X] = lo_of(c1); }
             }
-            if (p.outS) {   // snapshot of u^{n+TK}
+            if (SAVE) {   // snapshot of u^{n+TK}
               float* os = p.outS + off;
               if (xin1) { if (yin0) sts64(os, o0); if (yin1) sts64(os + X, o1); }
               else { if (yin0) os[0] = lo_of(o0); if (yin1) os[X] = lo_of(o1); }
@@ -362,17 +388,18 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
   }
 }
 
-template <int L, int R, int TK, bool WAVE, int OY>
+template <int L, int R, int TK, bool WAVE, int OY, bool SAVE>
 __device__ __forceinline__ void dispatch_level(int l, const SweepParams& p, int nslot, uint32_t sbase,
                                                int warp, int lane, int tx0, int ty0, int zb, int ze) {
   if (l == L) {
-    level_warp<L, R, TK, WAVE, OY>(p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
+    level_warp<L, R, TK, WAVE, OY, SAVE>(p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
   } else if constexpr (L + 1 < TK) {
-    dispatch_level<L + 1, R, TK, WAVE, OY>(l, p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
+    dispatch_level<L + 1, R, TK, WAVE, OY, SAVE>(l, p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
   }
 }
 
-template <int R, int TK, bool WAVE, int OY>
+// SAVE: the pass also stores u^{n+TK} into the snapshot field p.outS (separate instance).
+template <int R, int TK, bool WAVE, int OY, bool SAVE>
 __global__ void __launch_bounds__(Geom2<R, TK, WAVE, OY>::NTHREADS, 1)
 sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ SweepParams p,
               const int nslot) {
@@ -454,7 +481,7 @@ sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
   int l = 0;
 #pragma unroll
   for (int m = 1; m < TK; ++m) l += (warp >= G::wbase(m)) ? 1 : 0;
-  dispatch_level<0, R, TK, WAVE, OY>(l, p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
+  dispatch_level<0, R, TK, WAVE, OY, SAVE>(l, p, nslot, sbase, warp, lane, tx0, ty0, zb, ze);
 }
 
 }  // namespace st

@@ -16,6 +16,9 @@ VARIANTS = {
     "de3dl4": dict(defines=["-DST_DE2=3", "-DST_DL2=4"]),
     "de4dl3": dict(defines=["-DST_DE2=4", "-DST_DL2=3"]),
     "de3dl5rot": dict(defines=["-DST_DE2=3", "-DST_DL2=5", "-DST_ROT2=1"]),
+    "w1": dict(defines=["-DST_WAIT2=1"]),
+    "w2": dict(defines=["-DST_WAIT2=2"]),
+    "w1dl3": dict(defines=["-DST_WAIT2=1", "-DST_DL2=3"]),
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
