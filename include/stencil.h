@@ -60,7 +60,12 @@ typedef enum {
   ST_ESTATE = 6           /* plan is in an error state after an asynchronous failure */
 } st_status;
 
-enum { ST_FTZ = 1u };     /* flush denormals (required; the only arithmetic mode built) */
+enum {
+  ST_FTZ = 1u,            /* flush denormals (required; the only arithmetic mode built) */
+  ST_NO_SWAP = 2u         /* stencil_run may return the pair swapped instead of launching a swap
+                             kernel (2 reads + 2 writes per point) after an odd number of in-place
+                             T = 1 passes; stencil_swapped() tells the caller (see there) */
+};
 
 typedef struct {
   int32_t ndim;           /* 2 or 3 */
@@ -75,7 +80,7 @@ typedef struct {
   int32_t rank, nranks;   /* z-slab index/count; n[2] % nranks == 0 */
   int32_t device;         /* CUDA device ordinal */
   void *stream;           /* cudaStream_t all work is enqueued on (NULL = legacy default) */
-  uint32_t flags;         /* ST_FTZ (must be set) */
+  uint32_t flags;         /* ST_FTZ (must be set) | ST_NO_SWAP (optional) */
 } st_config;
 
 /* Validate cfg, pick the compiled kernel instance, allocate scratch.  *out = NULL on error.
@@ -128,6 +133,12 @@ st_status stencil_run_save(stencil_plan *p, float *u_prev, float *u_cur, const f
                            const int32_t *src_xyz, const float *src_wavelet, int32_t nrec,
                            const int32_t *rec_xyz, float *rec_trace, int32_t save_every,
                            float *snapshots, int64_t snap_stride);
+
+/* 1 if the last stencil_run / stencil_run_save of p (created with ST_NO_SWAP) left the pair
+ * swapped: u_prev then holds u^{n+nt} and u_cur holds u^{n+nt-1}, and the caller exchanges its two
+ * references before the next run.  0 otherwise (always 0 without ST_NO_SWAP); -1 if p is NULL.
+ * Used by the z-slab runner, which advances T_c = 1 step per call (an odd pass count every call). */
+int32_t stencil_swapped(const stencil_plan *p);
 
 /* Wait for the plan's stream; surfaces asynchronous CUDA errors (then ST_ECUDA, and the plan
  * enters ST_ESTATE). */

@@ -13,13 +13,14 @@ LIB_PATH = os.environ.get("ST_LIB") or os.path.join(HERE, "libstencil.so")   # S
 
 ST_OK, ST_EINVAL, ST_ENOMEM, ST_ECUDA, ST_EUNSUPPORTED, ST_ESTATE = 0, 1, 2, 3, 5, 6
 ST_FTZ = 1
+ST_NO_SWAP = 2
 STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 5: "ST_EUNSUPPORTED",
                 6: "ST_ESTATE"}
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_run_save", "stencil_sync",
            "stencil_destroy", "stencil_last_error", "stencil_supported", "stencil_abi_version",
-           "stencil_set_timing", "stencil_timing")
+           "stencil_set_timing", "stencil_timing", "stencil_swapped")
 
 
 class StConfig(ctypes.Structure):
@@ -83,6 +84,8 @@ def load():
     lib.stencil_timing.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
     lib.stencil_timing.restype = ctypes.c_int
+    lib.stencil_swapped.argtypes = [P]
+    lib.stencil_swapped.restype = ctypes.c_int32
     lib.stencil_abi_version.argtypes = []
     lib.stencil_abi_version.restype = ctypes.c_int32
     _lib = lib

@@ -55,6 +55,7 @@ struct stencil_plan {
   // scratch
   Buf ac, p2, c2, tables;
   Buf staging;       // pinned host staging for the src/rec tables
+  bool last_swapped = false;           // ST_NO_SWAP: the last run returned the pair swapped
   bool have_medium = false;            // a/c hold the medium of an earlier run (vel == NULL reuses it)
   bool have_tables = false;            // tables hold the src/rec lists below (re-uploaded on change)
   std::vector<int32_t> last_src, last_rec;
@@ -231,7 +232,9 @@ struct Tables {
 
 extern "C" {
 
-int32_t stencil_abi_version(void) { return 102; }
+int32_t stencil_abi_version(void) { return 103; }
+
+int32_t stencil_swapped(const stencil_plan* p) { return p ? (p->last_swapped ? 1 : 0) : -1; }
 
 int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel) {
   return st::find_kernel(ndim, time_order, radius, t_kernel) != nullptr ? 1 : 0;
@@ -645,8 +648,11 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
 
   // honour the contract: (u_prev, u_cur) buffers hold (u^{n+nt-1}, u^{n+nt})
   const size_t field_bytes = (size_t)plane * p->Z * 4;
+  p->last_swapped = false;
   if (prev == 0 && cur == 1) {
     // done
+  } else if (prev == 1 && cur == 0 && (c.flags & ST_NO_SWAP)) {
+    p->last_swapped = true;            // the caller exchanges its references (stencil_swapped)
   } else if (prev == 1 && cur == 0) {
     const long long n4 = (long long)(field_bytes / 16);
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)p->sm_count * 8);

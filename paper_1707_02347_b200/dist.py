@@ -114,7 +114,7 @@ class SlabRunner:
         self.device = device
         self.stencil = Stencil(problem.ndim, problem.n, problem.space_order, problem.time_order,
                                problem.dt, problem.dx, t_kernel=t_kernel, t_comm=self.tc, rank=rank,
-                               nranks=world, device=device)
+                               nranks=world, device=device, no_swap=True)
         st = self.stencil
         self.G = st.G
         self.nzl = st.nz_local
@@ -224,6 +224,8 @@ class SlabRunner:
                    damp=dev.get("damp") if first else None,
                    step0=done, src=list(p.src), wavelet=dev.get("wavelet"), rec=list(p.rec),
                    trace=None if trace is None else trace[done:done + n])
+            if st.swapped():      # odd pass count (T_c = 1): swap references, not 2 fields of HBM
+                dev["u_prev"], dev["u_cur"] = dev["u_cur"], dev["u_prev"]
             done += n
         if trace is not None and self.world > 1:
             dist.all_reduce(trace)

@@ -36,7 +36,7 @@ class Stencil:
     def __init__(self, ndim: int, n: Sequence[int], space_order: int, time_order: int, dt: float,
                  dx: Sequence[float], t_kernel: int = 1, t_comm: int = 1, rank: int = 0,
                  nranks: int = 1, device: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None,
-                 coeffs: Optional[Sequence[float]] = None):
+                 coeffs: Optional[Sequence[float]] = None, no_swap: bool = False):
         lib = _lib.load()
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -57,7 +57,7 @@ class Stencil:
         cfg.rank, cfg.nranks = int(rank), int(nranks)
         cfg.device = self.device
         cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
-        cfg.flags = _lib.ST_FTZ
+        cfg.flags = _lib.ST_FTZ | (_lib.ST_NO_SWAP if no_swap else 0)
         self._cfg = cfg
         h = ctypes.c_void_p()
         _lib.check(lib.stencil_create(ctypes.byref(cfg), ctypes.byref(h)))
@@ -132,6 +132,11 @@ class Stencil:
             st = lib.stencil_run(*args)
         _lib.check(st, self._h)
         return trace
+
+    def swapped(self) -> bool:
+        """no_swap plans: True if the last run left (u_prev, u_cur) holding (u^{n+nt}, u^{n+nt-1});
+        the caller then exchanges its two references (include/stencil.h stencil_swapped)."""
+        return _lib.load().stencil_swapped(self._h) == 1
 
     def set_timing(self, enable: bool = True):
         _lib.check(_lib.load().stencil_set_timing(self._h, int(enable)), self._h)

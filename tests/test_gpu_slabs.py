@@ -21,14 +21,14 @@ def _problem(order=8, nz=48):
                                 (33, 20, nz // 4))})
 
 
-def _run_slabs(p, world, tk, tc):
+def _run_slabs(p, world, tk, tc, no_swap=False):
     from paper_1707_02347_b200 import Stencil
     from paper_1707_02347_b200.dist import local_exchange
     plans, fields = [], []
     wav = torch.from_numpy(W.wavelet(p)).cuda()
     for rk in range(world):
         st = Stencil(p.ndim, p.n, p.space_order, p.time_order, p.dt, p.dx, t_kernel=tk, t_comm=tc,
-                     rank=rk, nranks=world)
+                     rank=rk, nranks=world, no_swap=no_swap)
         has_lo, has_hi = rk > 0, rk < world - 1
         z0 = st.z_range[0]
         lo = z0 - (st.G if has_lo else 0)
@@ -49,8 +49,13 @@ def _run_slabs(p, world, tk, tc):
         n = min(tc, p.nt - done)
         local_exchange(fields, G, nzl, p.radius, n, need_prev=True)
         for st, f in zip(plans, fields):
-            st.run(f["u_prev"], f["u_cur"], n, vel=f["vel"], damp=f["damp"], step0=done,
+            first = done == 0           # later chunks reuse the plan's medium (vel = NULL)
+            st.run(f["u_prev"], f["u_cur"], n, vel=f["vel"] if first else None,
+                   damp=f["damp"] if first else None, step0=done,
                    src=list(p.src), wavelet=wav, rec=list(p.rec), trace=f["trace"][done:done + n])
+            if st.swapped():            # no_swap plans: exchange references, as SlabRunner does
+                assert no_swap
+                f["u_prev"], f["u_cur"] = f["u_cur"], f["u_prev"]
         done += n
     torch.cuda.synchronize()
     P = np.concatenate([st.interior(f["u_prev"]).cpu().numpy() for st, f in zip(plans, fields)])
@@ -68,6 +73,17 @@ def test_emulated_slabs_bitwise(world, tk, tc):
     got = _run_slabs(p, world, tk, tc)
     want = oracle.run_problem(p)
     assert np.abs(want[1]).max() > 0
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("world,tk,tc", [(2, 1, 1), (4, 1, 1), (3, 2, 2), (2, 1, 3)])
+def test_emulated_slabs_no_swap(world, tk, tc):
+    """SlabRunner's mode: no_swap plans (odd pass counts return the pair swapped, the caller swaps
+    references), medium derived on the first chunk only."""
+    p = _problem()
+    got = _run_slabs(p, world, tk, tc, no_swap=True)
+    want = oracle.run_problem(p)
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
 
