@@ -145,11 +145,13 @@ def run_gpu(args):
     else:
         tc = tk
     nt = p.nt if args.nt is None else args.nt
-    runner = SlabRunner(p, rank=rank, world=world, t_kernel=tk, t_comm=tc, device=local)
+    runner = SlabRunner(p, rank=rank, world=world, t_kernel=tk, t_comm=tc, device=local,
+                        fused=args.fused_halo)
     st = runner.stencil
     # ---- host inputs (pinned) for this rank's slab, then resident device copies ----------------
     host = runner.host_inputs(nt, pin=True)
     dev_in = runner.to_device(host)
+    fused = runner.enable_fused(dev_in) if args.fused_halo else False
 
     def step_resident():
         runner.reset_state(dev_in)          # zero initial fields (device memset, part of the step)
@@ -234,6 +236,9 @@ def run_gpu(args):
                 "time_order": p.time_order, "t_kernel": tk, "t_comm": tc if world > 1 else None,
                 "schedule": pl.reason if args.tk == "auto" else f"t_kernel={tk} forced by --tk (planner: {pl.reason})",
                 "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                "halo": (None if world == 1 else
+                         "fused push: sweep stores band planes into peer ghost zones (P2P)" if fused
+                         else "NCCL send/recv of contiguous ghost planes every T_c steps"),
                 "l2": "inputs larger than L2 (fields %.0f MiB each, L2 126 MB); no flush" % (
                     runner.field_bytes / 2**20),
             },
@@ -371,6 +376,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=2, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused-halo", action="store_true",
+                    help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")
     args = ap.parse_args()
     _OVERRIDE.update(so=args.so, n=args.grid)
     if args.warmup < 3:

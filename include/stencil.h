@@ -140,6 +140,39 @@ st_status stencil_run_save(stencil_plan *p, float *u_prev, float *u_cur, const f
  * Used by the z-slab runner, which advances T_c = 1 step per call (an odd pass count every call). */
 int32_t stencil_swapped(const stencil_plan *p);
 
+/* ---- Fused halo push -------------------------------
+ * For z-slab plans with t_comm == t_kernel == 1 and ST_NO_SWAP, the halo exchange can be fused
+ * into the sweep: each T = 1 pass stores its r lowest (highest) owned output planes, besides
+ * locally, straight into the lo (hi) neighbour's ghost zone over peer memory (NVLink P2P), then
+ * the CTAs that pushed bump the neighbour's inbound counter (release, system scope); before the
+ * TMA loads of its ghost planes the next pass waits until its own counters show the neighbours'
+ * pushes of the previous step (acquire, system scope).  No NCCL call and no copy per step.
+ * The ranks must issue identical run sequences (nt == 1 each) on identically configured plans;
+ * the ghost planes of the first run come from the caller (initial state or one NCCL exchange).
+ * Peer device pointers come from the same process (another plan of this process) or from
+ * stencil_ipc_open of a blob a peer process made with stencil_ipc_export. */
+
+/* This plan's two inbound push counters (device u64 [2]: [0] from the lo neighbour, [1] from the
+ * hi neighbour), allocated and zeroed on the first call; the neighbours register them. */
+st_status stencil_peer_counters(stencil_plan *p, unsigned long long **counters);
+
+/* Register the neighbour on `side` (0 = rank-1, 1 = rank+1): my_a/my_b are this rank's two field
+ * buffers (the u_prev/u_cur pair, in either order later), peer_a/peer_b the neighbour's
+ * corresponding buffers (its my_a/my_b) and peer_counters its stencil_peer_counters.  Every
+ * existing side must be registered before a run is fused; each registration restarts the step
+ * count.  ST_EINVAL: not a fused-capable plan (see above), no neighbour on that side, null or
+ * aliased pointers, a my_a/my_b pair differing from the other side's. */
+st_status stencil_set_peer(stencil_plan *p, int32_t side, const float *my_a, const float *my_b,
+                           float *peer_a, float *peer_b, unsigned long long *peer_counters);
+
+#define ST_IPC_BYTES 72
+/* Export the device allocation holding dev_ptr for another process: blob (ST_IPC_BYTES) receives
+ * a cudaIpcMemHandle_t of the allocation's base and the offset of dev_ptr in it. */
+st_status stencil_ipc_export(const stencil_plan *p, const void *dev_ptr, void *blob);
+/* Open a blob from stencil_ipc_export in this process: *dev_ptr = base + offset.  The plan
+ * closes the handle when it is destroyed. */
+st_status stencil_ipc_open(stencil_plan *p, const void *blob, void **dev_ptr);
+
 /* Wait for the plan's stream; surfaces asynchronous CUDA errors (then ST_ECUDA, and the plan
  * enters ST_ESTATE). */
 st_status stencil_sync(stencil_plan *p);

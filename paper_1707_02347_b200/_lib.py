@@ -20,7 +20,9 @@ STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 5: "S
 # Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_run_save", "stencil_sync",
            "stencil_destroy", "stencil_last_error", "stencil_supported", "stencil_abi_version",
-           "stencil_set_timing", "stencil_timing", "stencil_swapped")
+           "stencil_set_timing", "stencil_timing", "stencil_swapped", "stencil_peer_counters",
+           "stencil_set_peer", "stencil_ipc_export", "stencil_ipc_open")
+ST_IPC_BYTES = 72
 
 
 class StConfig(ctypes.Structure):
@@ -84,6 +86,14 @@ def load():
     lib.stencil_timing.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
     lib.stencil_timing.restype = ctypes.c_int
+    lib.stencil_peer_counters.argtypes = [P, ctypes.POINTER(P)]
+    lib.stencil_peer_counters.restype = ctypes.c_int
+    lib.stencil_set_peer.argtypes = [P, ctypes.c_int32, P, P, P, P, P]
+    lib.stencil_set_peer.restype = ctypes.c_int
+    lib.stencil_ipc_export.argtypes = [P, P, P]
+    lib.stencil_ipc_export.restype = ctypes.c_int
+    lib.stencil_ipc_open.argtypes = [P, P, ctypes.POINTER(P)]
+    lib.stencil_ipc_open.restype = ctypes.c_int
     lib.stencil_swapped.argtypes = [P]
     lib.stencil_swapped.restype = ctypes.c_int32
     lib.stencil_abi_version.argtypes = []

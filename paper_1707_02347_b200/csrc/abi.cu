@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -56,6 +57,13 @@ struct stencil_plan {
   Buf ac, p2, c2, tables;
   Buf staging;       // pinned host staging for the src/rec tables
   bool last_swapped = false;           // ST_NO_SWAP: the last run returned the pair swapped
+  // fused halo push (stencil_set_peer)
+  Buf counters;                        // 2 x u64 inbound push counters: [0] from lo, [1] from hi
+  const float* my_ab[2] = {nullptr, nullptr};          // this rank's two field buffers
+  float* peer_ab[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][a/b] peer buffers
+  unsigned long long* peer_ctr[2] = {nullptr, nullptr};              // neighbours' counters
+  long long fused_runs = 0;            // fused runs issued since the peers were set
+  std::vector<void*> ipc_opened;       // handles opened by stencil_ipc_open (closed on destroy)
   bool have_medium = false;            // a/c hold the medium of an earlier run (vel == NULL reuses it)
   bool have_tables = false;            // tables hold the src/rec lists below (re-uploaded on change)
   std::vector<int32_t> last_src, last_rec;
@@ -232,9 +240,88 @@ struct Tables {
 
 extern "C" {
 
-int32_t stencil_abi_version(void) { return 103; }
+int32_t stencil_abi_version(void) { return 104; }
 
 int32_t stencil_swapped(const stencil_plan* p) { return p ? (p->last_swapped ? 1 : 0) : -1; }
+
+// ------------------------------------------------------------------ fused halo push (NEXT-1)
+static bool fused_capable(const stencil_plan* p) {
+  const st_config& c = p->cfg;
+  return c.ndim == 3 && c.nranks > 1 && c.t_comm == 1 && c.t_kernel == 1;
+}
+
+static bool fused_ready(const stencil_plan* p) {
+  return fused_capable(p) && p->my_ab[0] && (!p->has_lo || p->peer_ctr[0]) && (!p->has_hi || p->peer_ctr[1]);
+}
+
+st_status stencil_peer_counters(stencil_plan* p, unsigned long long** counters) {
+  if (!p || !counters) return fail(p, ST_EINVAL, "plan or counters is NULL");
+  CK(cudaSetDevice(p->device), "cudaSetDevice");
+  if (!p->counters.ptr) {
+    st_status s = ensure_buf(p, p->counters, 2 * sizeof(unsigned long long), "push counters");
+    if (s != ST_OK) return s;
+    CK(cudaMemset(p->counters.ptr, 0, 2 * sizeof(unsigned long long)), "cudaMemset counters");
+  }
+  *counters = static_cast<unsigned long long*>(p->counters.ptr);
+  return ST_OK;
+}
+
+st_status stencil_set_peer(stencil_plan* p, int32_t side, const float* my_a, const float* my_b,
+                           float* peer_a, float* peer_b, unsigned long long* peer_counters) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  if (!fused_capable(p)) return fail(p, ST_EINVAL, "fused halo push needs ndim 3, nranks > 1, t_comm == t_kernel == 1");
+  if (!(p->cfg.flags & ST_NO_SWAP))
+    return fail(p, ST_EINVAL, "fused halo push needs a ST_NO_SWAP plan (a swap kernel would race with the peers' pushes)");
+  if (side != 0 && side != 1) return fail(p, ST_EINVAL, "side must be 0 (lo) or 1 (hi)");
+  if ((side == 0 && !p->has_lo) || (side == 1 && !p->has_hi)) return fail(p, ST_EINVAL, "rank has no neighbour on side %d", side);
+  if (!my_a || !my_b || my_a == my_b || !peer_a || !peer_b || !peer_counters)
+    return fail(p, ST_EINVAL, "null or aliased buffer / counter pointer");
+  if (p->my_ab[0] && (p->my_ab[0] != my_a || p->my_ab[1] != my_b))
+    return fail(p, ST_EINVAL, "my_a/my_b differ from the pair registered for the other side");
+  unsigned long long* mine = nullptr;
+  st_status s = stencil_peer_counters(p, &mine);       // make sure ours exist (the peer bumps them)
+  if (s != ST_OK) return s;
+  p->my_ab[0] = my_a; p->my_ab[1] = my_b;
+  p->peer_ab[side][0] = peer_a; p->peer_ab[side][1] = peer_b;
+  p->peer_ctr[side] = peer_counters;
+  p->fused_runs = 0;
+  return ST_OK;
+}
+
+st_status stencil_ipc_export(const stencil_plan* p, const void* dev_ptr, void* blob) {
+  if (!p || !dev_ptr || !blob) return fail(nullptr, ST_EINVAL, "null argument");
+  if (cudaSetDevice(p->device) != cudaSuccess) return fail(nullptr, ST_ECUDA, "cudaSetDevice failed");
+  // base of the allocation holding dev_ptr (torch's caching allocator sub-allocates segments)
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+    return fail(nullptr, ST_ECUDA, "cuMemGetAddressRange lookup failed");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn)(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+    return fail(nullptr, ST_ECUDA, "cuMemGetAddressRange failed for %p", dev_ptr);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+  if (e != cudaSuccess) return fail(nullptr, ST_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  const long long off = (long long)((CUdeviceptr)dev_ptr - base);
+  memcpy(blob, &h, sizeof h);
+  memcpy(static_cast<char*>(blob) + 64, &off, sizeof off);
+  return ST_OK;
+}
+
+st_status stencil_ipc_open(stencil_plan* p, const void* blob, void** dev_ptr) {
+  if (!p || !blob || !dev_ptr) return fail(p, ST_EINVAL, "null argument");
+  CK(cudaSetDevice(p->device), "cudaSetDevice");
+  cudaIpcMemHandle_t h;
+  long long off = 0;
+  memcpy(&h, blob, sizeof h);
+  memcpy(&off, static_cast<const char*>(blob) + 64, sizeof off);
+  void* base = nullptr;
+  CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  p->ipc_opened.push_back(base);
+  *dev_ptr = static_cast<char*>(base) + off;
+  return ST_OK;
+}
 
 int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int32_t t_kernel) {
   return st::find_kernel(ndim, time_order, radius, t_kernel) != nullptr ? 1 : 0;
@@ -353,6 +440,8 @@ void stencil_destroy(stencil_plan* p) {
   if (p->staging.ptr) cudaFreeHost(p->staging.ptr);
   if (p->staging_ev) cudaEventDestroy(p->staging_ev);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  for (void* h : p->ipc_opened) cudaIpcCloseMemHandle(h);
+  free_buf(p->counters);
   delete p;
 }
 
@@ -508,6 +597,11 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
       return fail(p, ST_EINVAL, "receiver %d (%d,%d,%d) outside the interior", i, q[0], q[1], q[2]);
   }
   if (nt == 0) return ST_OK;
+  // fused halo push: every run is one T = 1 pass whose output field is one of the registered pair
+  const bool fused = fused_ready(p);
+  if (fused && u_prev != p->my_ab[0] && u_prev != p->my_ab[1])
+    return fail(p, ST_EINVAL, "fused halo push: u_prev is neither of the buffers given to stencil_set_peer");
+  if (fused && save_every > 0) return fail(p, ST_EINVAL, "fused halo push does not combine with snapshots");
   int aux_launches = 0;
   CK(cudaSetDevice(p->device), "cudaSetDevice");
 
@@ -633,6 +727,42 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
     const int chunks = choose_chunks(p, k, bps, tiles, planes);
     sp.zchunk = (int)((planes + chunks - 1) / chunks);
     dim3 grid((unsigned)((p->nx + k->ox - 1) / k->ox), (unsigned)((p->ny + k->oy - 1) / k->oy), (unsigned)chunks);
+    sp.push_lo = sp.push_hi = nullptr;
+    sp.band_lo = INT_MIN; sp.band_hi = INT_MAX;
+    sp.sig_lo = sp.sig_hi = nullptr;
+    sp.wait_lo = sp.wait_hi = nullptr;
+    sp.wait_lo_target = sp.wait_hi_target = 0;
+    if (fused) {
+      // the band planes of u^{n+1} go straight into the neighbours' ghost zones (their output
+      // field of this step, which corresponds to ours: the ranks advance in lockstep)
+      const int ob = (sp.outP == p->my_ab[0]) ? 0 : 1;
+      const int r = c.radius;
+      // CTAs whose chunk produces band planes (identical geometry on every rank)
+      long long n_lo = 0, n_hi = 0;
+      for (int ch = 0; ch < chunks; ++ch) {
+        const long long zb = sp.out_lo + (long long)ch * sp.zchunk, ze = std::min<long long>(sp.out_hi, zb + sp.zchunk);
+        if (zb >= ze) continue;
+        if (zb < sp.out_lo + r) ++n_lo;
+        if (ze > sp.out_hi - r) ++n_hi;
+      }
+      n_lo *= tiles; n_hi *= tiles;
+      unsigned long long* mine = static_cast<unsigned long long*>(p->counters.ptr);
+      if (p->has_lo) {
+        sp.push_lo = p->peer_ab[0][ob] + p->nzl * plane;     // my planes [G, G+r) -> its [G+nzl, ...)
+        sp.band_lo = sp.out_lo + r;
+        sp.sig_lo = p->peer_ctr[0] + 1;                       // "from hi" on the lo neighbour
+        sp.wait_lo = mine + 0;                                // the lo neighbour pushed its hi band
+        sp.wait_lo_target = (unsigned long long)(p->fused_runs * n_hi);
+      }
+      if (p->has_hi) {
+        sp.push_hi = p->peer_ab[1][ob] - p->nzl * plane;     // my planes [G+nzl-r, G+nzl) -> its [G-r, G)
+        sp.band_hi = sp.out_hi - r;
+        sp.sig_hi = p->peer_ctr[1] + 0;
+        sp.wait_hi = mine + 1;
+        sp.wait_hi_target = (unsigned long long)(p->fused_runs * n_lo);
+      }
+      ++p->fused_runs;
+    }
     CK(k->launch(km, sp, grid, nslot, smem, p->stream), "sweep kernel launch");
     ++launches;
     tiled_launches += tiled ? 1 : 0;

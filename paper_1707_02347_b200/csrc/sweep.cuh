@@ -55,6 +55,22 @@ struct SweepParams {
   float* trace;               // [run step][nrec_total]
   int tr_stride;
   int tr_step;                // run-relative step index of level 0 of this pass
+  // fused halo push (z-slabs, T_c = T_k = 1).  Output planes
+  // s < band_lo are also stored at push_lo + (same offset) -- the lo neighbour's output field,
+  // pre-shifted by +nzl planes so the store lands in its upper ghost zone; s >= band_hi at
+  // push_hi (pre-shifted by -nzl planes, the hi neighbour's lower ghost zone).  A CTA that pushed
+  // adds 1 to sig_lo / sig_hi (the neighbour's inbound counter) after its stores, release at
+  // system scope.  Before the TMA load of a ghost plane below out_lo (above out_hi) the producer
+  // waits until *wait_lo >= wait_lo_target (*wait_hi >= wait_hi_target), acquire at system scope.
+  // All pointers nullptr (band_lo = INT_MIN, band_hi = INT_MAX) when not fused.
+  float* push_lo;
+  float* push_hi;
+  int band_lo, band_hi;
+  unsigned long long* sig_lo;
+  unsigned long long* sig_hi;
+  const unsigned long long* wait_lo;
+  const unsigned long long* wait_hi;
+  unsigned long long wait_lo_target, wait_hi_target;
 };
 
 // Tensor maps of one launch: u = u^n box with halo (every kernel); the time-tiled kernel's
@@ -128,6 +144,56 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                  : "=r"(ok) : "r"(a), "r"(parity) : "memory");
   } while (!ok);
 }
+// ---- fused halo push: cross-GPU signalling (system scope)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* a, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" :: "l"(a), "l"(v) : "memory");
+}
+// Wait until a neighbour's pushes of the previous step have landed, then order the later TMA
+// (async-proxy) reads of the ghost planes after that acquire.
+// A neighbour that never signals (a mismatched run sequence) must not hang the GPU: after ~20 s
+// the kernel traps, the run fails with ST_ECUDA and the plan enters ST_ESTATE.
+__device__ __forceinline__ void wait_peer(const unsigned long long* ctr, unsigned long long target) {
+  if (ld_acquire_sys(ctr) < target) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(ctr) < target) {
+      __nanosleep(256);
+      if (clock64() - t0 > 40000000000ll) __trap();
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Producer side of every untiled kernel: before the TMA load of array plane z.
+__device__ __forceinline__ void wait_ghost(const SweepParams& p, int z, bool& lo_done, bool& hi_done) {
+#ifdef ST_NO_PUSH
+  return;
+#endif
+  if (!lo_done && z < p.out_lo) {
+    if (p.wait_lo) wait_peer(p.wait_lo, p.wait_lo_target);
+    lo_done = true;
+  }
+  if (!hi_done && z >= p.out_hi) {
+    if (p.wait_hi) wait_peer(p.wait_hi, p.wait_hi_target);
+    hi_done = true;
+  }
+}
+// Consumer side, after the CTA's last step: every pushing thread fences its peer stores, the
+// consumer warps meet at named barrier 1, one thread bumps the neighbours' counters.
+__device__ __forceinline__ void signal_peers(const SweepParams& p, bool pushed_lo, bool pushed_hi,
+                                             int nconsumer_threads) {
+  if (!(pushed_lo || pushed_hi)) return;   // CTA-uniform
+  __threadfence_system();
+  asm volatile("bar.sync 1, %0;" :: "r"(nconsumer_threads) : "memory");
+  if (threadIdx.x == 0) {
+    if (pushed_lo) red_release_sys_add(p.sig_lo, 1ull);
+    if (pushed_hi) red_release_sys_add(p.sig_hi, 1ull);
+  }
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2) {
   asm volatile(

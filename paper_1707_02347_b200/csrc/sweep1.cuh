@@ -132,8 +132,10 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmapC)) : "memory");
       int slot = 0;
       uint32_t ph = 0;
+      bool lo_done = false, hi_done = false;
       for (int a = 0; a < n_arr; ++a) {
         if (a >= nslot) mbar_wait(&empty[slot], ph ^ 1u);
+        wait_ghost(p, p_first + a, lo_done, hi_done);   // fused halo: neighbour's push landed
         mbar_expect_tx(&full[slot], (uint32_t)(BW * G::BH * 4));
         tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &full[slot], tx0 - RXB, ty0 - R,
                     p_first + a - p.zv_lo);
@@ -161,6 +163,14 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   const bool act = any_row && xin0;               // this lane owns >= 1 interior point
   // warp-uniform: every row and column of this warp is interior (the common case) -> plain stores
   const bool whole = (tx0 + 64 <= p.nx) && (y0 + VY <= p.ny);
+  // fused halo push (CTA-uniform): this chunk produces planes of the lo / hi band
+  const bool push_lo = p.push_lo != nullptr && zb < p.band_lo;
+  const bool push_hi = p.push_hi != nullptr && ze > p.band_hi;
+#ifdef ST_NO_PUSH
+  const bool push_any = false;     // experiment: the fused-push code compiled out
+#else
+  const bool push_any = push_lo || push_hi;
+#endif
   const int col = (warp * VY + R) * BW + 2 * lane + RXB;   // my first row's pair in a ring slot
   const uint64_t DT = splat(p.dt);
   // rare events of this warp's rows (sources / receivers), decided once per CTA chunk
@@ -263,24 +273,25 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
 #pragma unroll
             for (int j = 0; j < VY; ++j) o[j] = f2fma(DT, acc[j], qn[md<QN>(u - RZ)][j]) & mask[j];
           }
-          if (whole) {
+          auto put = [&](float* d) {       // whole tile: plain stores; ragged: masked
+            if (whole) {
 #pragma unroll
-            for (int j = 0; j < VY; ++j) {
-              sts64(out + j * X, o[j]);
-              if (SAVE) sts64(outs + j * X, o[j]);
-            }
-          } else if (act) {
+              for (int j = 0; j < VY; ++j) sts64(d + j * X, o[j]);
+            } else if (act) {
 #pragma unroll
-            for (int j = 0; j < VY; ++j) {
-              if (yin[j]) {
-                if (xin1) sts64(out + j * X, o[j]);
-                else out[j * X] = lo_of(o[j]);
-                if (SAVE) {
-                  if (xin1) sts64(outs + j * X, o[j]);
-                  else outs[j * X] = lo_of(o[j]);
+              for (int j = 0; j < VY; ++j) {
+                if (yin[j]) {
+                  if (xin1) sts64(d + j * X, o[j]);
+                  else d[j * X] = lo_of(o[j]);
                 }
               }
             }
+          };
+          put(out);
+          if (SAVE) put(outs);
+          if (push_any) {                    // fused halo: band planes also into the neighbour's ghosts
+            if (s < p.band_lo) put(p.push_lo + (out - p.outP));
+            if (s >= p.band_hi) put(p.push_hi + (out - p.outP));
           }
           if (wrec) {
 #pragma unroll
@@ -303,6 +314,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     }
   }
   if (WAVE) cp_async_wait<0>();
+  signal_peers(p, push_lo, push_hi, 32 * NCW);
 }
 
 }  // namespace st

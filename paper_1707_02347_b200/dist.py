@@ -105,7 +105,7 @@ class SlabRunner:
     planes every T_c steps.  world == 1 degenerates to a single stencil_run per simulation."""
 
     def __init__(self, problem, rank: int = 0, world: int = 1, t_kernel: int = 1, t_comm: int = 1,
-                 device: int = 0):
+                 device: int = 0, fused: bool = False):
         from .stencil import Stencil
         self.p = problem
         self.rank, self.world = rank, world
@@ -123,6 +123,9 @@ class SlabRunner:
         self.field_bytes = st.X * st.Y * st.Z * 4
         self.wave = problem.time_order == 2
         self._timing = False
+        # fused halo push (include/stencil.h): T_c = T_k = 1 only; enabled by enable_fused()
+        self.fused_capable = fused and world > 1 and t_kernel == 1 and self.tc == 1
+        self.fused = False
 
     @property
     def nz_local(self):
@@ -166,6 +169,27 @@ class SlabRunner:
             dev["trace"] = torch.zeros((max(1, self.p.nt), len(self.p.rec)), dtype=torch.float32,
                                        device=f"cuda:{self.device}")
         return dev
+
+    def enable_fused(self, dev, group=None):
+        """Fused halo push: every rank exports (IPC) its two field buffers and its inbound
+        counters, all-gathers the blobs over the process group and registers its z-neighbours'
+        with the library; from then on a run's sweep stores its band planes straight into the
+        neighbours' ghost zones and only the first chunk of each simulation calls NCCL."""
+        if not self.fused_capable:
+            return False
+        st = self.stencil
+        a, b = dev["u_prev"], dev["u_cur"]
+        mine = (st.ipc_export(a.data_ptr()), st.ipc_export(b.data_ptr()),
+                st.ipc_export(st.peer_counters()))
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, mine, group=group)
+        for side, peer in ((0, self.rank - 1), (1, self.rank + 1)):
+            if 0 <= peer < self.world:
+                pa, pb, pc = (st.ipc_open(x) for x in blobs[peer])
+                st.set_peer(side, a, b, pa, pb, pc)
+        dist.barrier(group=group)
+        self.fused = True
+        return True
 
     def reset_state(self, dev):
         dev["u_cur"].copy_(dev["_init_cur"])
@@ -215,7 +239,9 @@ class SlabRunner:
         done = 0
         while done < nt:
             n = min(self.tc, nt - done) if self.world > 1 else nt - done
-            if self.world > 1:
+            # fused: the sweeps push the ghost planes themselves; NCCL only before the first step
+            # (it also orders this simulation's reset after the neighbours' last pushes)
+            if self.world > 1 and (not self.fused or done == 0):
                 halo_exchange(dev, self.rank, self.world, self.G, self.nzl, p.radius, n,
                               need_prev=self.wave)
             # the medium a, c is derived once per simulation (first chunk); later chunks reuse it

@@ -138,6 +138,34 @@ class Stencil:
         the caller then exchanges its two references (include/stencil.h stencil_swapped)."""
         return _lib.load().stencil_swapped(self._h) == 1
 
+    # ------------------------------------------------------------------ fused halo push
+    def peer_counters(self) -> int:
+        """Device address of this plan's two inbound push counters (include/stencil.h)."""
+        c = ctypes.c_void_p()
+        _lib.check(_lib.load().stencil_peer_counters(self._h, ctypes.byref(c)), self._h)
+        return int(c.value)
+
+    def set_peer(self, side: int, my_a: torch.Tensor, my_b: torch.Tensor, peer_a: int, peer_b: int,
+                 peer_counters: int):
+        """Register the neighbour on `side` (0 = rank-1, 1 = rank+1) for the fused halo push:
+        my_a/my_b this rank's field pair, peer_* device addresses valid in this process."""
+        _lib.check(_lib.load().stencil_set_peer(self._h, int(side), _ptr(my_a), _ptr(my_b),
+                                                ctypes.c_void_p(peer_a), ctypes.c_void_p(peer_b),
+                                                ctypes.c_void_p(peer_counters)), self._h)
+
+    def ipc_export(self, ptr: int) -> bytes:
+        """IPC blob (handle of the allocation holding device address ptr + offset)."""
+        blob = ctypes.create_string_buffer(_lib.ST_IPC_BYTES)
+        _lib.check(_lib.load().stencil_ipc_export(self._h, ctypes.c_void_p(ptr), blob), self._h)
+        return blob.raw
+
+    def ipc_open(self, blob: bytes) -> int:
+        """Device address in this process of a peer process's exported pointer."""
+        out = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(bytes(blob), _lib.ST_IPC_BYTES)
+        _lib.check(_lib.load().stencil_ipc_open(self._h, buf, ctypes.byref(out)), self._h)
+        return int(out.value)
+
     def set_timing(self, enable: bool = True):
         _lib.check(_lib.load().stencil_set_timing(self._h, int(enable)), self._h)
 

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_host_queries():
     lib = _lib.load()
-    assert lib.stencil_abi_version() == 103
+    assert lib.stencil_abi_version() == 104
     for r in range(1, 9):
         for to in (1, 2):
             assert lib.stencil_supported(3, to, r, 1) == 1

@@ -88,6 +88,90 @@ def test_emulated_slabs_no_swap(world, tk, tc):
         assert np.array_equal(g, w)
 
 
+def _run_fused(p, world, steps_per_sim=None, sims=1):
+    """Fused halo push on one GPU: N no_swap slab plans whose peers are the other plans' buffers
+    (same process), run one step each in rank order.  The initial ghost planes come from the
+    seeded global fields (embedded with the slab's ghosts); there is no exchange call at all.
+    sims > 1 repeats the simulation from the initial state with the same plans (the counters keep
+    counting, as in the bench's warm-up + timed simulations)."""
+    from paper_1707_02347_b200 import Stencil
+    plans, fields, init = [], [], []
+    wav = torch.from_numpy(W.wavelet(p)).cuda()
+    for rk in range(world):
+        st = Stencil(p.ndim, p.n, p.space_order, p.time_order, p.dt, p.dx, t_kernel=1, t_comm=1,
+                     rank=rk, nranks=world, no_swap=True)
+        z0 = st.z_range[0]
+        lo = z0 - (st.G if rk > 0 else 0)
+        hi = z0 + st.nz_local + (st.G if rk < world - 1 else 0)
+        gl = z0 - lo
+        f = {}
+        up, uc = W.initial_fields(p, lo, hi)
+        f["u_prev"] = st.embed(torch.from_numpy(up).cuda(), ghost_lo=gl)
+        f["u_cur"] = st.embed(torch.from_numpy(uc).cuda(), ghost_lo=gl)
+        f["vel"] = st.embed(torch.from_numpy(W.velocity(p, lo, hi)).cuda(), ghost_lo=gl)
+        f["damp"] = st.embed(torch.from_numpy(W.damp(p, lo, hi)).cuda(), ghost_lo=gl)
+        f["trace"] = torch.zeros((p.nt, len(p.rec)), dtype=torch.float32, device="cuda")
+        init.append((f["u_prev"].clone(), f["u_cur"].clone()))
+        plans.append(st)
+        fields.append(f)
+    ab = [(f["u_prev"], f["u_cur"]) for f in fields]
+    for rk, st in enumerate(plans):
+        for side, peer in ((0, rk - 1), (1, rk + 1)):
+            if 0 <= peer < world:
+                st.set_peer(side, ab[rk][0], ab[rk][1], ab[peer][0].data_ptr(), ab[peer][1].data_ptr(),
+                            plans[peer].peer_counters())
+    for sim in range(sims):
+        for f, (ip, ic) in zip(fields, init):
+            f["u_prev"].copy_(ip)
+            f["u_cur"].copy_(ic)
+            f["trace"].zero_()
+        for n in range(p.nt):
+            for st, f in zip(plans, fields):
+                st.run(f["u_prev"], f["u_cur"], 1, vel=f["vel"] if n == 0 else None,
+                       damp=f["damp"] if n == 0 else None, step0=n, src=list(p.src), wavelet=wav,
+                       rec=list(p.rec), trace=f["trace"][n:n + 1])
+                if st.swapped():
+                    f["u_prev"], f["u_cur"] = f["u_cur"], f["u_prev"]
+    torch.cuda.synchronize()
+    P = np.concatenate([st.interior(f["u_prev"]).cpu().numpy() for st, f in zip(plans, fields)])
+    C = np.concatenate([st.interior(f["u_cur"]).cpu().numpy() for st, f in zip(plans, fields)])
+    T = sum(f["trace"] for f in fields).cpu().numpy()
+    for st in plans:
+        st.close()
+    return P, C, T
+
+
+@pytest.mark.parametrize("world,order,sims", [(2, 8, 1), (3, 12, 1), (4, 4, 2), (4, 16, 1)])
+def test_fused_halo_push_bitwise(world, order, sims):
+    """NEXT-1: the sweep stores its band planes straight into the neighbours' ghost zones and
+    signals them; the next step's producer waits for the counters.  Bit-exact vs the oracle."""
+    p = _problem(order=order, nz=48)
+    got = _run_fused(p, world, sims=sims)
+    want = oracle.run_problem(p)
+    assert np.abs(want[1]).max() > 0
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_fused_halo_push_rejects_bad_plans():
+    from paper_1707_02347_b200 import Stencil
+    from paper_1707_02347_b200._lib import StencilError
+    p = _problem()
+    st = Stencil(3, p.n, 8, 2, p.dt, p.dx, t_kernel=1, t_comm=1, rank=0, nranks=2)   # no no_swap
+    a, b = st.empty(), st.empty()
+    with pytest.raises(StencilError, match="ST_NO_SWAP"):
+        st.set_peer(1, a, b, a.data_ptr(), b.data_ptr(), st.peer_counters())
+    st.close()
+    st = Stencil(3, p.n, 8, 2, p.dt, p.dx, t_kernel=1, t_comm=2, rank=0, nranks=2, no_swap=True)
+    with pytest.raises(StencilError, match="t_comm"):
+        st.set_peer(1, a, b, a.data_ptr(), b.data_ptr(), st.peer_counters())
+    st.close()
+    st = Stencil(3, p.n, 8, 2, p.dt, p.dx, t_kernel=1, t_comm=1, rank=0, nranks=2, no_swap=True)
+    with pytest.raises(StencilError, match="neighbour"):
+        st.set_peer(0, a, b, a.data_ptr(), b.data_ptr(), st.peer_counters())   # rank 0 has no lo
+    st.close()
+
+
 def test_ghost_deeper_than_slab_rejected():
     from paper_1707_02347_b200 import Stencil
     from paper_1707_02347_b200._lib import ST_EINVAL, StencilError

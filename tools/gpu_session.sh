@@ -34,6 +34,11 @@ if [[ $what == all || $what == ncu ]]; then
   timeout 300 $CMD > $O/plain_prof_c5.log 2>&1 &&
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep -s 2 -c 1 \
       -o $O/prof_C5_tk1 -f $CMD > $O/ncu_c5.log 2>&1
+  # untiled C4 (SO16, T=1)
+  CMD="python tools/prof_run.py --config C4 --tk 1 --nt 4"
+  timeout 300 $CMD > $O/plain_prof_c4.log 2>&1 &&
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep -s 2 -c 1 \
+      -o $O/prof_C4_tk1 -f $CMD > $O/ncu_c4.log 2>&1
   # time-tiled C3 (SO8, T_k=2)
   CMD="python tools/prof_run.py --config C3 --tk 2 --nt 6"
   timeout 300 $CMD > $O/plain_prof_c3.log 2>&1 &&
