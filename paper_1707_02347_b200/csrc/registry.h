@@ -76,20 +76,30 @@ template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t launch_sweep1(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
   if (p.outS)
-    sweep1_kernel<R, WAVE, NDIM, NCW, VY, true><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
-  else
-    sweep1_kernel<R, WAVE, NDIM, NCW, VY, false><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+    sweep1_kernel<R, WAVE, NDIM, NCW, VY, 1><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  else if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi) {
+    if constexpr (NDIM == 3)
+      sweep1_kernel<R, WAVE, NDIM, NCW, VY, 2><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+    else
+      return cudaErrorNotSupported;
+  } else
+    sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
   return cudaGetLastError();
 }
 
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t query_sweep1(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweep1_kernel<R, WAVE, NDIM, NCW, VY, false>;
+  auto k = sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(sweep1_kernel<R, WAVE, NDIM, NCW, VY, true>,
+  e = cudaFuncSetAttribute(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 1>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if constexpr (NDIM == 3) {
+    e = cudaFuncSetAttribute(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   if (attr) {
     e = cudaFuncGetAttributes(attr, k);
     if (e != cudaSuccess) return e;
@@ -111,20 +121,23 @@ template <int R, bool WAVE, int NCW, int VY>
 cudaError_t launch_sweep1s(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                            size_t smem, cudaStream_t stream) {
   if (p.outS)
-    sweep1s_kernel<R, WAVE, NCW, VY, true><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+    sweep1s_kernel<R, WAVE, NCW, VY, 1><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+  else if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi)
+    sweep1s_kernel<R, WAVE, NCW, VY, 2><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
   else
-    sweep1s_kernel<R, WAVE, NCW, VY, false><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+    sweep1s_kernel<R, WAVE, NCW, VY, 0><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
   return cudaGetLastError();
 }
 
 template <int R, bool WAVE, int NCW, int VY>
 cudaError_t query_sweep1s(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweep1s_kernel<R, WAVE, NCW, VY, false>;
+  auto k = sweep1s_kernel<R, WAVE, NCW, VY, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(sweep1s_kernel<R, WAVE, NCW, VY, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  for (auto kk : {sweep1s_kernel<R, WAVE, NCW, VY, 1>, sweep1s_kernel<R, WAVE, NCW, VY, 2>}) {
+    e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   if (attr) {
     e = cudaFuncGetAttributes(attr, k);
     if (e != cudaSuccess) return e;

@@ -169,9 +169,6 @@ __device__ __forceinline__ void wait_peer(const unsigned long long* ctr, unsigne
 }
 // Producer side of every untiled kernel: before the TMA load of array plane z.
 __device__ __forceinline__ void wait_ghost(const SweepParams& p, int z, bool& lo_done, bool& hi_done) {
-#ifdef ST_NO_PUSH
-  return;
-#endif
   if (!lo_done && z < p.out_lo) {
     if (p.wait_lo) wait_peer(p.wait_lo, p.wait_lo_target);
     lo_done = true;

@@ -92,12 +92,15 @@ __device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent,
   return false;
 }
 
-// SAVE: this pass also stores u^{n+1} into the snapshot field p.outS (stencil_run_save); a separate
-// instance, so the plain sweep carries no snapshot logic in its step body.
-template <int R, bool WAVE, int NDIM, int NCW, int VY, bool SAVE>
+// MODE 0: plain sweep.  MODE 1 (SAVE): this pass also stores u^{n+1} into the snapshot field
+// p.outS (stencil_run_save).  MODE 2 (PUSH): fused halo push (band planes into the neighbours'
+// ghost zones, producer waits for theirs).  Separate instances, so the plain sweep carries no
+// snapshot or push logic in its step body (measured: the push checks cost C4 11 %).
+template <int R, bool WAVE, int NDIM, int NCW, int VY, int MODE>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
 sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
               const int nslot) {
+  constexpr bool SAVE = MODE == 1, PUSH = MODE == 2;
   using G = Geom1<R, NDIM, NCW, VY>;
   constexpr int RZ = G::RZ, QN = G::QN, RX2 = G::RX2, RXB = G::RXB, BW = G::BW;
   constexpr int SLOT_F = G::SLOT_BYTES / 4;
@@ -135,7 +138,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       bool lo_done = false, hi_done = false;
       for (int a = 0; a < n_arr; ++a) {
         if (a >= nslot) mbar_wait(&empty[slot], ph ^ 1u);
-        wait_ghost(p, p_first + a, lo_done, hi_done);   // fused halo: neighbour's push landed
+        if (PUSH) wait_ghost(p, p_first + a, lo_done, hi_done);   // neighbour's push landed
         mbar_expect_tx(&full[slot], (uint32_t)(BW * G::BH * 4));
         tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &full[slot], tx0 - RXB, ty0 - R,
                     p_first + a - p.zv_lo);
@@ -164,13 +167,9 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   // warp-uniform: every row and column of this warp is interior (the common case) -> plain stores
   const bool whole = (tx0 + 64 <= p.nx) && (y0 + VY <= p.ny);
   // fused halo push (CTA-uniform): this chunk produces planes of the lo / hi band
-  const bool push_lo = p.push_lo != nullptr && zb < p.band_lo;
-  const bool push_hi = p.push_hi != nullptr && ze > p.band_hi;
-#ifdef ST_NO_PUSH
-  const bool push_any = false;     // experiment: the fused-push code compiled out
-#else
+  const bool push_lo = PUSH && p.push_lo != nullptr && zb < p.band_lo;
+  const bool push_hi = PUSH && p.push_hi != nullptr && ze > p.band_hi;
   const bool push_any = push_lo || push_hi;
-#endif
   const int col = (warp * VY + R) * BW + 2 * lane + RXB;   // my first row's pair in a ring slot
   const uint64_t DT = splat(p.dt);
   // rare events of this warp's rows (sources / receivers), decided once per CTA chunk
@@ -289,7 +288,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
           };
           put(out);
           if (SAVE) put(outs);
-          if (push_any) {                    // fused halo: band planes also into the neighbour's ghosts
+          if (PUSH && push_any) {            // fused halo: band planes also into the neighbour's ghosts
             if (s < p.band_lo) put(p.push_lo + (out - p.outP));
             if (s >= p.band_hi) put(p.push_hi + (out - p.outP));
           }
@@ -314,7 +313,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     }
   }
   if (WAVE) cp_async_wait<0>();
-  signal_peers(p, push_lo, push_hi, 32 * NCW);
+  if (PUSH) signal_peers(p, push_lo, push_hi, 32 * NCW);
 }
 
 }  // namespace st

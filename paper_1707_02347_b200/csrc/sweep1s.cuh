@@ -38,10 +38,12 @@ struct Geom1S {
   static constexpr int FIXED_BYTES = BAR_BYTES + (WAVE ? stage_bytes(PD) : 0);
 };
 
-template <int R, bool WAVE, int NCW, int VY, bool SAVE>
+// MODE: 0 plain, 1 snapshot store (SAVE), 2 fused halo push (PUSH), as sweep1_kernel.
+template <int R, bool WAVE, int NCW, int VY, int MODE>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
 sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
                const int nslot_unused) {
+  constexpr bool SAVE = MODE == 1, PUSH = MODE == 2;
   using G = Geom1<R, 3, NCW, VY>;
   using S = Geom1S<R, NCW, VY, WAVE>;
   static_assert(S::OK, "static ring does not fit in shared memory");
@@ -82,7 +84,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
       bool lo_done = false, hi_done = false;
       for (int a = 0; a < n_arr; ++a) {
         if (a >= NS) mbar_wait(&empty[slot], ph ^ 1u);
-        wait_ghost(p, p_first + a, lo_done, hi_done);   // fused halo: neighbour's push landed
+        if (PUSH) wait_ghost(p, p_first + a, lo_done, hi_done);   // neighbour's push landed
         mbar_expect_tx(&full[slot], (uint32_t)(BW * G::BH * 4));
         tma_load_3d(ring + (size_t)slot * SLOT_F, &tmapC, &full[slot], tx0 - RXB, ty0 - R,
                     p_first + a - p.zv_lo);
@@ -109,13 +111,9 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
   const bool act = any_row && xin0;
   const bool whole = (tx0 + 64 <= p.nx) && (y0 + VY <= p.ny);   // warp-uniform: plain stores
   // fused halo push (CTA-uniform): this chunk produces planes of the lo / hi band
-  const bool push_lo = p.push_lo != nullptr && zb < p.band_lo;
-  const bool push_hi = p.push_hi != nullptr && ze > p.band_hi;
-#ifdef ST_NO_PUSH
-  const bool push_any = false;     // experiment: the fused-push code compiled out
-#else
+  const bool push_lo = PUSH && p.push_lo != nullptr && zb < p.band_lo;
+  const bool push_hi = PUSH && p.push_hi != nullptr && ze > p.band_hi;
   const bool push_any = push_lo || push_hi;
-#endif
   const float* rcol = ring + (warp * VY + R) * BW + 2 * lane + RXB;   // my pair, slot 0
   const uint64_t DT = splat(p.dt);
   bool wsrc = false, wrec = false;
@@ -206,7 +204,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
     };
     put(out);
     if (SAVE) put(outs);
-    if (push_any) {                    // fused halo: band planes also into the neighbour's ghosts
+    if (PUSH && push_any) {            // fused halo: band planes also into the neighbour's ghosts
       if (s < p.band_lo) put(p.push_lo + (out - p.outP));
       if (s >= p.band_hi) put(p.push_hi + (out - p.outP));
     }
@@ -254,7 +252,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
     ph ^= 1u;
   }
   if (WAVE) cp_async_wait<0>();
-  signal_peers(p, push_lo, push_hi, 32 * NCW);
+  if (PUSH) signal_peers(p, push_lo, push_hi, 32 * NCW);
 }
 
 }  // namespace st

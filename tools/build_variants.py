@@ -17,7 +17,6 @@ VARIANTS = {
     "de4dl3": dict(defines=["-DST_DE2=4", "-DST_DL2=3"]),
     "de3dl5rot": dict(defines=["-DST_DE2=3", "-DST_DL2=5", "-DST_ROT2=1"]),
     "w1": dict(defines=["-DST_WAIT2=1"]),
-    "nopush": dict(defines=["-DST_NO_PUSH"]),
     "w2": dict(defines=["-DST_WAIT2=2"]),
     "w1dl3": dict(defines=["-DST_WAIT2=1", "-DST_DL2=3"]),
 }
