@@ -188,7 +188,8 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
     return _build(BUILD, LIB, jobs=jobs, verbose=verbose)
 
 
-def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = True) -> str:
+def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = True,
+                  static_r=None) -> str:
     """Experimental library _variants/libstencil_<name>.so with extra -D flags and (optionally)
     only the instances whose (ndim, wave, R, TK) is listed; load it with ST_LIB=<path>."""
     inst = instances()
@@ -197,6 +198,9 @@ def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = Tru
     outdir = os.path.join(HERE, "_variants", name)
     os.makedirs(os.path.join(HERE, "_varlib"), exist_ok=True)
     lib = os.path.join(HERE, "_varlib", f"libstencil_{name}.so")   # shipped to the GPU box
+    if static_r is not None:   # radii whose 3-D untiled instances use the static ring (kind 3)
+        inst = [i[:6] + ((3 if i[2] in static_r else 1),) if i[0] == 3 and i[3] == 1 and i[6] in (1, 3)
+                else i for i in inst]
     if t1 is not None:   # (consumer warps, rows per warp) of the untiled kernel
         inst = [i[:4] + (t1[1], t1[0], 1) if i[6] == 1 else i for i in inst]
     return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose)
