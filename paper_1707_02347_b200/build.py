@@ -51,7 +51,12 @@ def _sweep2_oy(wave: int, R: int, TK: int):
     """Output rows of the sweep2 (one warp group per level) instance, or None if it does not fit
     (<= 31 consumer warps of two rows; wave only two levels)."""
     if TK == 2 and R <= 4:
-        return 16 if R < 3 else 14      # <= 20 warps incl. 2 producers (96 registers/thread)
+        # measured (DESIGN.md §10, 512^3 x 200 steps, GPts/s): wave SO2 OY 16/14/12/10/8 ->
+        # 381/416/423/372/332; SO4 16/14/12/10 -> 355/379/359/300; SO6 16/14/12 -> 255/255/248;
+        # SO8 14/12/10 -> 219/224/188; heat R = 1 16/12/10/8... -> 575/497/676 (two CTAs per SM)
+        if wave:
+            return {1: 12, 2: 14, 3: 16, 4: 12}[R]
+        return 10 if R == 1 else 16
     if not wave and TK == 4 and R <= 2:
         return 8
     return None
@@ -189,7 +194,7 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
 
 
 def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = True,
-                  static_r=None) -> str:
+                  static_r=None, oy2=None) -> str:
     """Experimental library _variants/libstencil_<name>.so with extra -D flags and (optionally)
     only the instances whose (ndim, wave, R, TK) is listed; load it with ST_LIB=<path>."""
     inst = instances()
@@ -198,6 +203,8 @@ def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = Tru
     outdir = os.path.join(HERE, "_variants", name)
     os.makedirs(os.path.join(HERE, "_varlib"), exist_ok=True)
     lib = os.path.join(HERE, "_varlib", f"libstencil_{name}.so")   # shipped to the GPU box
+    if oy2 is not None:        # {(wave, R, TK): OY} output rows of time-tiled (kind 2) instances
+        inst = [i[:5] + (oy2.get((i[1], i[2], i[3]), i[5]),) + i[6:] if i[6] == 2 else i for i in inst]
     if static_r is not None:   # radii whose 3-D untiled instances use the static ring (kind 3)
         inst = [i[:6] + ((3 if i[2] in static_r else 1),) if i[0] == 3 and i[3] == 1 and i[6] in (1, 3)
                 else i for i in inst]

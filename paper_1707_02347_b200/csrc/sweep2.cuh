@@ -400,7 +400,10 @@ __device__ __forceinline__ void dispatch_level(int l, const SweepParams& p, int 
 
 // SAVE: the pass also stores u^{n+TK} into the snapshot field p.outS (separate instance).
 template <int R, int TK, bool WAVE, int OY, bool SAVE>
-__global__ void __launch_bounds__(Geom2<R, TK, WAVE, OY>::NTHREADS, 1)
+#ifndef ST_MINB2
+#define ST_MINB2 1      // experiment: resident CTAs per SM the register allocation must allow
+#endif
+__global__ void __launch_bounds__(Geom2<R, TK, WAVE, OY>::NTHREADS, ST_MINB2)
 sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ SweepParams p,
               const int nslot) {
   using G = Geom2<R, TK, WAVE, OY>;
