@@ -73,12 +73,12 @@ class Plan:
 # Measured on B200 (512^3 x 200 steps unless noted): GPts/s of the untiled and the
 # two-level kernels; 0 = not compiled as the warp-group kernel / not measured.
 _MEASURED = {  # (time_order, radius): (T=1, T_k=2)
-    (2, 1): (330, 382), (2, 2): (330, 361), (2, 3): (331, 264), (2, 4): (324, 216),
-    (2, 5): (305, 0),   # between SO8 and SO12 (estimate)
-    (2, 6): (260, 0),   # C5 768^3 x 2000 (bench)
+    (2, 1): (332, 423), (2, 2): (330, 378), (2, 3): (316, 266), (2, 4): (318, 226),
+    (2, 5): (300, 0),   # between SO8 and SO12 (estimate)
+    (2, 6): (285, 0),   # C5 768^3 x 2000 (bench, sweep1s)
     (2, 7): (256, 0),   # SO14 study run
-    (2, 8): (233, 0),   # C4 1024^3 x 1000 (bench)
-    (1, 1): (736, 590), (1, 2): (700, 0),
+    (2, 8): (245, 0),   # C4 1024^3 x 1000 (bench)
+    (1, 1): (708, 677), (1, 2): (700, 0),
 }
 NVLINK_GBS = 770.0          # measured peer copy per direction (B200_PROFILING.md)
 EXCHANGE_LATENCY_US = 25.0  # NCCL send/recv launch + sync per exchange (estimate)
