@@ -247,7 +247,7 @@ def run_gpu(args):
             "gpu_launches": int(sweep_launches + aux),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "st::sweep_kernel", "alg_bytes_per_point_launch": bpp,
+                         "kernel": _kernel_name(p, tk), "alg_bytes_per_point_launch": bpp,
                          "per_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src},
             "clocks": ck,
         }
@@ -270,6 +270,16 @@ def _describe(p: W.Problem) -> str:
             + (f", {len(p.src)} Ricker source(s) {p.f_peak:g} Hz" if p.src else "")
             + (f", {len(p.rec)} receivers" if p.rec else "")
             + (f", {p.sponge}-pt sponge" if p.sponge else ""))
+
+
+def _kernel_name(p: W.Problem, tk: int) -> str:
+    """Name of the compiled sweep instance a pass of this problem launches (build.instances())."""
+    from paper_1707_02347_b200.build import instances
+    names = {0: "st::sweep_kernel", 1: "st::sweep1_kernel", 2: "st::sweep2_kernel", 3: "st::sweep1s_kernel"}
+    for (ndim, wave, R, TK, VY, NWY, kind) in instances():
+        if (ndim, wave, R, TK) == (p.ndim, int(p.time_order == 2), p.radius, tk):
+            return f"{names[kind]}<R={R}, T_k={TK}>"
+    return "st::sweep_kernel"
 
 
 def _ncu_traffic(cfg: str, tk: int):
