@@ -194,7 +194,7 @@ constexpr KernelEntry make_entry2() {
   return KernelEntry{3, WAVE ? 2 : 1, R, TK, 2, G::NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                      R, (size_t)G::SLOT_BYTES, (size_t)G::FIXED_BYTES,
                      &launch_sweep2<R, TK, WAVE, OY>, &query_sweep2<R, TK, WAVE, OY>, ST_T2_DEPTH,
-                     WAVE ? G::EBW : 0, WAVE ? G::GH : 0, WAVE ? G::OY : 0, G::NSLOT_FIX};
+                     WAVE ? G::EBW : 0, WAVE ? G::GH : 0, WAVE ? G::OY : 0};
 }
 
 }  // namespace st

@@ -119,14 +119,7 @@ struct Geom2 {
 #ifndef ST_DL2
 #define ST_DL2 2
 #endif
-#ifndef ST_STATIC2
-#define ST_STATIC2 0    // experiment: TMA ring and level ring of U slots, compile-time indices
-#endif
-  // static rings: U = a multiple of QN with >= 7 slots; ring slot of step a = a mod U, queue
-  // entry a mod QN -- both constants of the U-fold unrolled step body
-  static constexpr int U = ST_STATIC2 ? QN * (QN >= 7 ? 1 : (7 + QN - 1) / QN) : QN;
-  static constexpr int NSLOT_FIX = ST_STATIC2 ? U : 0;     // host must launch with nslot = U
-  static constexpr int DL = ST_STATIC2 ? U : R + ST_DL2;   // level-ring depth (planes); >= R + 1
+  static constexpr int DL = R + ST_DL2;            // level-ring depth (planes); >= R + 1 needed
   static constexpr int LVL_BYTES = GW * (GH + 2 * R) * 4;   // one plane + R pad rows each side
 #ifndef ST_DE2
 #define ST_DE2 0        // 0: as deep as shared memory allows (below)
@@ -144,8 +137,7 @@ struct Geom2 {
   // E-ring depth: as deep as the shared memory left after the level rings and a u^n ring of
   // R + 3 slots allows (2..8); measured: deeper E rings hide the DRAM latency of the medium.
   static constexpr int SMEM_MAX = 227 * 1024;
-  static constexpr int DE_FIT = (SMEM_MAX - 2048 - (TK - 1) * DL * LVL_BYTES -
-                                 (ST_STATIC2 ? U : R + 3) * SLOT_BYTES) /
+  static constexpr int DE_FIT = (SMEM_MAX - 2048 - (TK - 1) * DL * LVL_BYTES - (R + 3) * SLOT_BYTES) /
                                 (E0_BYTES + E1_BYTES);
   static constexpr int DE = ST_DE2 ? ST_DE2 : (DE_FIT < 2 ? 2 : DE_FIT > 8 ? 8 : DE_FIT);
   static constexpr int BAR_BYTES = 2048;   // full[64] | empty[64] | lfull | lempty | E0 f/e | E1 f/e
@@ -277,36 +269,30 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
 
   // ST_ROT2 = 1: the z-queue is rotated by register moves after each step (code = one step
   // body); 0: the loop is unrolled by the queue length and the queue indexed modulo QN.
-  // ST_STATIC2: unrolled by U (ring size), every ring slot/parity is uu / the block parity
-  constexpr bool SR = ST_STATIC2 != 0;
-  constexpr int UNR = SR ? G::U : (ST_ROT2 ? 1 : QN);
-  uint32_t blk = 0;                                  // SR: parity of the current U-block
+  constexpr int UNR = ST_ROT2 ? 1 : QN;
 #pragma unroll 1
-  for (int base = 0; base < n_arr; base += UNR, blk ^= 1u) {
+  for (int base = 0; base < n_arr; base += UNR) {
 #pragma unroll
   for (int uu = 0; uu < UNR; ++uu) {
     const int a = base + uu;
     if (a >= n_arr) break;
-    const int iN = SR ? md<QN>(uu) : (ST_ROT2 ? QN - 1 : uu);        // queue index of the newest plane
-    const int iC = SR ? md<QN>(uu - R) : (ST_ROT2 ? R : md<QN>(uu - R));   // ... of the centre plane
-    const int s_in = SR ? uu : in_slot;
-    const uint32_t ph_in = SR ? blk : in_ph;
+    const int iN = ST_ROT2 ? QN - 1 : uu;            // queue index of the newest plane
+    const int iC = ST_ROT2 ? R : md<QN>(uu - R);     // queue index of the centre plane
     // ---- input plane of step a into the queue ----------------------------------------------
     if (L == 0) {
-      mb_wait(b_full + 8 * s_in, ph_in);
-      const uint32_t s = ring_in + s_in * SLOT + my_in;
+      mb_wait(b_full + 8 * in_slot, in_ph);
+      const uint32_t s = ring_in + in_slot * SLOT + my_in;
       q[iN][0] = ld_s64<0>(s);
       q[iN][1] = ld_s64<PB>(s);
       // never a centre plane: release now, once this lane's loads from the slot have returned
-      if ((SR ? (uu < R && base == 0) : (a < R)))
-        mb_arrive(b_empty + 8 * s_in + (zero_after(q[iN][0], p.zero) | zero_after(q[iN][1], p.zero)));
-      if (!SR && ++in_slot == nslot) { in_slot = 0; in_ph ^= 1u; }
+      if (a < R) mb_arrive(b_empty + 8 * in_slot + (zero_after(q[iN][0], p.zero) | zero_after(q[iN][1], p.zero)));
+      if (++in_slot == nslot) { in_slot = 0; in_ph ^= 1u; }
     } else {
-      mb_wait(lf_in + 8 * s_in, ph_in);
-      const uint32_t s = ring_in + s_in * LVL + my_in;
+      mb_wait(lf_in + 8 * in_slot, in_ph);
+      const uint32_t s = ring_in + in_slot * LVL + my_in;
       q[iN][0] = ld_s64<0>(s);
       q[iN][1] = ld_s64<PB>(s);
-      if (!SR && ++in_slot == DL) { in_slot = 0; in_ph ^= 1u; }
+      if (++in_slot == DL) { in_slot = 0; in_ph ^= 1u; }
     }
     // ---- this step's E entry (wave) ----------------------------------------------------------
     if (WAVE) mb_wait(e_full + 8 * e_slot, e_ph);
@@ -314,11 +300,10 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
     // ---- level L at plane p_first + a - (L+1)R ----------------------------------------------
     uint64_t o0 = 0ull, o1 = 0ull;
     const bool centre = (L == 0) ? (a >= 2 * R) : (a >= R);
-    const int s_c = SR ? md<G::U>(uu - R) : c_slot;     // centre slot (arrival / step a - R)
     if (centre) {
       if (a >= a_lo && a < a_hi) {
         const int qp = p_first + a - (L + 1) * R;
-        const uint32_t cb = ring_in + s_c * ((L == 0) ? SLOT : LVL) + my_in;
+        const uint32_t cb = ring_in + c_slot * ((L == 0) ? SLOT : LVL) + my_in;
         uint64_t acc[2];
         accum2<R, PB>(acc, q, cb, p, iC);
         if (wsrc) {
@@ -372,11 +357,11 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
       }
       // release the centre plane
       if (L == 0) {
-        mb_arrive(b_empty + 8 * s_c);
-        if (!SR && ++c_slot == nslot) c_slot = 0;
+        mb_arrive(b_empty + 8 * c_slot);
+        if (++c_slot == nslot) c_slot = 0;
       } else {
-        mb_arrive(le_in + 8 * s_c);
-        if (!SR && ++c_slot == DL) c_slot = 0;
+        mb_arrive(le_in + 8 * c_slot);
+        if (++c_slot == DL) c_slot = 0;
       }
     }
     if (WAVE) {
@@ -386,13 +371,12 @@ __device__ __forceinline__ void level_warp(const SweepParams& p, const int nslot
 
     // ---- publish level L's plane into its ring (levels below the last) -----------------------
     if (L < TK - 1) {
-      const int s_o = SR ? uu : out_slot;
-      if (SR ? (base > 0) : (a >= DL)) mb_wait(le_out + 8 * s_o, (SR ? blk : out_ph) ^ 1u);
-      const uint32_t d = ring_out + s_o * LVL + my_out;
+      if (a >= DL) mb_wait(le_out + 8 * out_slot, out_ph ^ 1u);
+      const uint32_t d = ring_out + out_slot * LVL + my_out;
       st_s64(d, o0);
       st_s64(d + GW * 4, o1);
-      mb_arrive(lf_out + 8 * s_o);
-      if (!SR && ++out_slot == DL) { out_slot = 0; out_ph ^= 1u; }
+      mb_arrive(lf_out + 8 * out_slot);
+      if (++out_slot == DL) { out_slot = 0; out_ph ^= 1u; }
     }
 
     // ---- rotate the z-queue -------------------------------------------------------------------
