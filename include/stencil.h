@@ -160,8 +160,10 @@ st_status stencil_peer_counters(stencil_plan *p, unsigned long long **counters);
  * buffers (the u_prev/u_cur pair, in either order later), peer_a/peer_b the neighbour's
  * corresponding buffers (its my_a/my_b) and peer_counters its stencil_peer_counters.  Every
  * existing side must be registered before a run is fused; each registration restarts the step
- * count.  ST_EINVAL: not a fused-capable plan (see above), no neighbour on that side, null or
- * aliased pointers, a my_a/my_b pair differing from the other side's. */
+ * count and zeroes this plan's inbound counter of that side (synchronously), so register only
+ * while no run is in flight on this rank or its neighbours (e.g. between a device sync and a
+ * barrier of all ranks).  ST_EINVAL: not a fused-capable plan (see above), no neighbour on that
+ * side, null or aliased pointers, a my_a/my_b pair differing from the other side's. */
 st_status stencil_set_peer(stencil_plan *p, int32_t side, const float *my_a, const float *my_b,
                            float *peer_a, float *peer_b, unsigned long long *peer_counters);
 

@@ -209,7 +209,7 @@ def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = Tru
         inst = [i[:6] + ((3 if i[2] in static_r else 1),) if i[0] == 3 and i[3] == 1 and i[6] in (1, 3)
                 else i for i in inst]
     if t1 is not None:   # (consumer warps, rows per warp) of the untiled kernel
-        inst = [i[:4] + (t1[1], t1[0], 1) if i[6] == 1 else i for i in inst]
+        inst = [i[:4] + (t1[1], t1[0], i[6]) if i[6] in (1, 3) else i for i in inst]
     return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose)
 
 

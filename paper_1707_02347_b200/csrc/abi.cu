@@ -284,6 +284,9 @@ st_status stencil_set_peer(stencil_plan* p, int32_t side, const float* my_a, con
   p->my_ab[0] = my_a; p->my_ab[1] = my_b;
   p->peer_ab[side][0] = peer_a; p->peer_ab[side][1] = peer_b;
   p->peer_ctr[side] = peer_counters;
+  // the step count restarts: so does this side's inbound counter (no pushes may be in flight)
+  CK(cudaMemsetAsync(mine + side, 0, sizeof(unsigned long long), p->stream), "cudaMemsetAsync counter");
+  CK(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
   p->fused_runs = 0;
   return ST_OK;
 }

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstddef>
+#include <utility>
 
 #include "sweep.cuh"
 #include "sweep1.cuh"
@@ -71,20 +72,39 @@ constexpr KernelEntry make_entry() {
                      &query_sweep<R, TK, WAVE, NDIM, VY, NWY>, 3};
 }
 
+#ifndef ST_PDL
+#define ST_PDL 1        // untiled sweeps launch with programmatic stream serialisation (sweep.cuh)
+#endif
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, int block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = ST_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // ---- warp-specialised untiled kernel (sweep1.cuh)
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t launch_sweep1(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
+  const int block = 32 * (NCW + 1);
   if (p.outS)
-    sweep1_kernel<R, WAVE, NDIM, NCW, VY, 1><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
-  else if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi) {
+    return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 1>, grid, block, smem, stream, maps.u, p, nslot);
+  if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi) {
     if constexpr (NDIM == 3)
-      sweep1_kernel<R, WAVE, NDIM, NCW, VY, 2><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
+      return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 2>, grid, block, smem, stream, maps.u, p, nslot);
     else
       return cudaErrorNotSupported;
-  } else
-    sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
-  return cudaGetLastError();
+  }
+  return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0>, grid, block, smem, stream, maps.u, p, nslot);
 }
 
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
@@ -120,13 +140,12 @@ constexpr KernelEntry make_entry1() {
 template <int R, bool WAVE, int NCW, int VY>
 cudaError_t launch_sweep1s(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                            size_t smem, cudaStream_t stream) {
+  const int block = 32 * (NCW + 1);
   if (p.outS)
-    sweep1s_kernel<R, WAVE, NCW, VY, 1><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
-  else if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi)
-    sweep1s_kernel<R, WAVE, NCW, VY, 2><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
-  else
-    sweep1s_kernel<R, WAVE, NCW, VY, 0><<<grid, 32 * (NCW + 1), smem, stream>>>(maps.u, p, nslot);
-  return cudaGetLastError();
+    return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 1>, grid, block, smem, stream, maps.u, p, nslot);
+  if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi)
+    return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 2>, grid, block, smem, stream, maps.u, p, nslot);
+  return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0>, grid, block, smem, stream, maps.u, p, nslot);
 }
 
 template <int R, bool WAVE, int NCW, int VY>
@@ -161,11 +180,9 @@ constexpr KernelEntry make_entry1s() {
 template <int R, int TK, bool WAVE, int OY>
 cudaError_t launch_sweep2(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  if (p.outS)
-    sweep2_kernel<R, TK, WAVE, OY, true><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(maps, p, nslot);
-  else
-    sweep2_kernel<R, TK, WAVE, OY, false><<<grid, Geom2<R, TK, WAVE, OY>::NTHREADS, smem, stream>>>(maps, p, nslot);
-  return cudaGetLastError();
+  constexpr int block = Geom2<R, TK, WAVE, OY>::NTHREADS;
+  if (p.outS) return launch_pdl(sweep2_kernel<R, TK, WAVE, OY, true>, grid, block, smem, stream, maps, p, nslot);
+  return launch_pdl(sweep2_kernel<R, TK, WAVE, OY, false>, grid, block, smem, stream, maps, p, nslot);
 }
 
 template <int R, int TK, bool WAVE, int OY>

@@ -144,6 +144,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                  : "=r"(ok) : "r"(a), "r"(parity) : "memory");
   } while (!ok);
 }
+// ---- programmatic dependent launch (PDL): a sweep launched with programmatic stream
+// serialisation may start while the previous kernel of the stream drains.  Every CTA lets the
+// next launch begin once it is running (launch_dependents) and, before touching any global data,
+// waits until the previous grid has completed and its memory is visible (wait).  Only the
+// prologue (barrier init, tensor-map prefetch) and the launch latency overlap the predecessor.
+__device__ __forceinline__ void pdl_prologue_done() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---- fused halo push: cross-GPU signalling (system scope)
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
   unsigned long long v;

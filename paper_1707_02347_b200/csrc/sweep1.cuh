@@ -128,6 +128,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_prologue_done();
 
   if (warp == NCW) {
     // ------------------------------------------------------------------ producer warp

@@ -74,6 +74,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_prologue_done();
 
   if (warp == NCW) {
     // ------------------------------------------------------------------ producer warp

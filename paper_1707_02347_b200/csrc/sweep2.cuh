@@ -437,6 +437,7 @@ sweep2_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_prologue_done();
 
   if (warp >= NCW) {
     // ------------------------------------------------------------------ producer warp
