@@ -647,6 +647,10 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   sp.ac = static_cast<const float4*>(p->ac.ptr);
   sp.K0 = p->K0; sp.dt = p->dtf;
   memcpy(sp.W, p->W, sizeof sp.W);
+  sp.iso = 1;
+  for (int k = 1; k <= c.radius; ++k)
+    for (int a = 1; a < c.ndim; ++a)
+      if (memcmp(&p->W[a][k], &p->W[0][k], sizeof(float)) != 0) sp.iso = 0;
   sp.src_begin = sbeg; sp.src = sarr; sp.wavelet = src_wavelet; sp.wl_stride = nsrc;
   sp.rec_begin = rbeg; sp.rec = rarr; sp.trace = rec_trace; sp.tr_stride = nrec;
 

@@ -96,7 +96,8 @@ __device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent,
 // p.outS (stencil_run_save).  MODE 2 (PUSH): fused halo push (band planes into the neighbours'
 // ghost zones, producer waits for theirs).  Separate instances, so the plain sweep carries no
 // snapshot or push logic in its step body (measured: the push checks cost C4 11 %).
-template <int R, bool WAVE, int NDIM, int NCW, int VY, int MODE>
+// ISO: isotropic-weight instance (see accumulate), launched when p.iso (3-D, r >= 7, MODE 0).
+template <int R, bool WAVE, int NDIM, int NCW, int VY, int MODE, bool ISO = false>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
 sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
               const int nslot) {
@@ -251,7 +252,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
           const int s = s0 + idx;
           const float* rp = ring + slot_s * SLOT_F + col;
           uint64_t acc[VY];
-          accumulate<R, RZ, QN, VY, NDIM, BW>(acc, qn, rp, p, md<QN>(u - RZ));
+          accumulate<R, RZ, QN, VY, NDIM, BW, ISO>(acc, qn, rp, p, md<QN>(u - RZ));
           if (wsrc) {
 #pragma unroll
             for (int j = 0; j < VY; ++j)

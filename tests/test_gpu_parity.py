@@ -74,6 +74,15 @@ def test_wave_orders_ragged(order, tk):
     _check(_wave("C3", n, 17, 8, order=order, src=src, rec=rec), t_kernel=tk)
 
 
+@pytest.mark.parametrize("order", [12, 14, 16])
+@pytest.mark.parametrize("dx", [(10.0, 10.0, 10.0), (10.0, 12.5, 8.0)])
+def test_wave_isotropic_and_anisotropic_weights(order, dx):
+    """The isotropic-weight instance (one weight per k, launched when the per-axis weights are
+    bitwise equal: r >= 7) and the general one (anisotropic spacing) both match the oracle."""
+    p = _wave("C3", (70, 50, 40), 9, 6, order=order, src=[(35, 25, 20)], rec=[(35, 25, 20), (3, 4, 5)])
+    _check(W.Problem(**{**p.__dict__, "dx": dx, "dt": 4e-4}))
+
+
 @pytest.mark.parametrize("tk", [1, 2])
 def test_wave_tiny_grid(tk):
     """Grid smaller than one tile in every direction."""
