@@ -67,7 +67,9 @@ def _static_ring(ndim: int, wave: int, R: int) -> bool:
     slot/queue indices): where 2r+1 slots leave >= 5 planes of prefetch and, with the cp.async
     staging, fit in shared memory (Geom1S::OK) -- and where it measured faster (C5 SO12: 285.5 vs
     274.4 GPts/s)."""
-    return ndim == 3 and R in (5, 6)   # R = 8 (PD 3): C4 246 vs 252 GPts/s with sweep1 -> sweep1
+    # R = 8 (staging depth 3): equal to sweep1 with per-axis weights (241 / 241), +3.4 % with the
+    # isotropic-weight instance (C4 254.3 vs 245.9 GPts/s, same-box A/B)
+    return ndim == 3 and R in (5, 6, 8)
 
 
 def instances():

@@ -154,6 +154,10 @@ cudaError_t launch_sweep1s(const KernelMaps& maps, const SweepParams& p, dim3 gr
     return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 1>, grid, block, smem, stream, maps.u, p, nslot);
   if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi)
     return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 2>, grid, block, smem, stream, maps.u, p, nslot);
+  if constexpr (R >= 7) {
+    if (p.iso)
+      return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0, true>, grid, block, smem, stream, maps.u, p, nslot);
+  }
   return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0>, grid, block, smem, stream, maps.u, p, nslot);
 }
 
@@ -164,6 +168,11 @@ cudaError_t query_sweep1s(size_t smem, cudaFuncAttributes* attr, int* bps, int n
   if (e != cudaSuccess) return e;
   for (auto kk : {sweep1s_kernel<R, WAVE, NCW, VY, 1>, sweep1s_kernel<R, WAVE, NCW, VY, 2>}) {
     e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if constexpr (R >= 7) {
+    e = cudaFuncSetAttribute(sweep1s_kernel<R, WAVE, NCW, VY, 0, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   if (attr) {

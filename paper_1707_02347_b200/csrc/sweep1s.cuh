@@ -13,7 +13,7 @@
 //   * block 0 (the r-plane warm-up below the chunk, which only loads) is peeled, so the steady
 //     blocks carry no warm-up conditions;
 //   * the ring depth QN leaves r planes of TMA prefetch beyond the r+1 planes in use (r >= 5).
-// Built for the 3-D wave and heat at r = 5, 6 (build.py _static_ring: there QN slots plus the
+// Built for the 3-D wave and heat at r = 5, 6, 8 (build.py _static_ring: there QN slots plus the
 // cp.async staging fit in shared memory and it measured faster); other shapes keep sweep1_kernel.
 #pragma once
 #include "sweep1.cuh"
@@ -39,7 +39,7 @@ struct Geom1S {
 };
 
 // MODE: 0 plain, 1 snapshot store (SAVE), 2 fused halo push (PUSH), as sweep1_kernel.
-template <int R, bool WAVE, int NCW, int VY, int MODE>
+template <int R, bool WAVE, int NCW, int VY, int MODE, bool ISO = false>
 __global__ void __launch_bounds__(32 * (NCW + 1), 1)
 sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
                const int nslot_unused) {
@@ -167,7 +167,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
   auto compute = [&](const int CS, const int s) {
     if (WAVE) stage_next();                       // plane s + PD
     uint64_t acc[VY];
-    accumulate<R, R, QN, VY, 3, BW>(acc, qn, rcol + CS * SLOT_F, p, CS);
+    accumulate<R, R, QN, VY, 3, BW, ISO>(acc, qn, rcol + CS * SLOT_F, p, CS);
     if (wsrc) {
 #pragma unroll
       for (int j = 0; j < VY; ++j)

@@ -50,4 +50,4 @@ def test_alg_bytes_and_kernel_names():
     assert bench._alg_bytes_per_point_launch(c2, False, 1) == 8
     assert bench._kernel_name(c5, 1).startswith("st::sweep1s_kernel<R=6")
     assert bench._kernel_name(W.problem("C3"), 2).startswith("st::sweep2_kernel<R=4")
-    assert bench._kernel_name(W.problem("C4"), 1).startswith("st::sweep1_kernel<R=8")
+    assert bench._kernel_name(W.problem("C4"), 1).startswith("st::sweep1s_kernel<R=8")
