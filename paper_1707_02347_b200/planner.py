@@ -77,7 +77,7 @@ _MEASURED = {  # (time_order, radius): (T=1, T_k=2)
     (2, 5): (300, 0),   # between SO8 and SO12 (estimate)
     (2, 6): (285, 0),   # C5 768^3 x 2000 (bench, sweep1s)
     (2, 7): (256, 0),   # SO14 study run
-    (2, 8): (245, 0),   # C4 1024^3 x 1000 (bench)
+    (2, 8): (254, 0),   # C4 1024^3 x 1000 (bench, sweep1s ISO)
     (1, 1): (708, 677), (1, 2): (700, 0),
 }
 NVLINK_GBS = 770.0          # measured peer copy per direction (B200_PROFILING.md)
