@@ -11,6 +11,8 @@ Contents
                            P:1682-1707 are 0.046208 x these).
   medium(vel, damp, dt)    a, c of the damped leapfrog, oracle.cpp.
   run_untiled(...)         O1, the plain untiled loop nest.
+  run_literal(...)         O1-literal: the paper's printed wave expression and term order
+                           (P:1678-1708), to bound fp32 order drift (reading Q8).
   run_skewed(...)          O2, the paper's skewed time-tiled schedule.
   embed/extract            oracle layout <-> interior arrays.
 
@@ -62,6 +64,10 @@ def _load():
         for nm in ("oracle_run_skewed_f32", "oracle_run_skewed_f64"):
             f = getattr(lib, nm)
             f.argtypes = common + [I, I, I, I, I]
+            f.restype = I
+        for nm in ("oracle_run_literal_f32", "oracle_run_literal_f64"):
+            f = getattr(lib, nm)
+            f.argtypes = [I, L, L, L, I, P, P, D, P, P, P, P, I, L, I, P, P, I, P, P, I]
             f.restype = I
         for nm in ("oracle_medium_f32", "oracle_medium_f64"):
             f = getattr(lib, nm)
@@ -191,6 +197,30 @@ def run_skewed(ndim, n, order, coeffs, h, time_order, dt, P, C, a=None, c=None, 
                 src, wavelet, rec, ftz, extra=(Tt, Tz, Ty, B, skew))
 
 
+def run_literal(ndim, n, order, coeffs, h, dt, P, C, vel, damp, nt=1, step0=0, src=(), wavelet=None,
+                rec=(), ftz=True):
+    """O1-literal: the wave update in the paper's printed expression and term order
+    (oracle.cpp), from vel/damp instead of a/c.  Isotropic spacing only."""
+    dtype = P.dtype
+    r = order // 2
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    src, rec = list(src or []), list(rec or [])
+    src_a, rec_a = _pts(src), _pts(rec)
+    if src:
+        wavelet = np.ascontiguousarray(wavelet, dtype=dtype)
+    trace = np.zeros((nt, max(len(rec), 1)), dtype=dtype)
+    vel = np.ascontiguousarray(vel, dtype=dtype)
+    damp = np.ascontiguousarray(damp, dtype=dtype)
+    fn = _load().oracle_run_literal_f32 if dtype == np.float32 else _load().oracle_run_literal_f64
+    rc = fn(ndim, n[0], n[1], n[2], r, _ptr(coeffs), _ptr(h), float(dt), _ptr(P), _ptr(C), _ptr(vel),
+            _ptr(damp), nt, step0, len(src), _ptr(src_a), _ptr(wavelet) if src else None, len(rec),
+            _ptr(rec_a), _ptr(trace), int(ftz))
+    if rc != 0:
+        raise ValueError(f"oracle_run_literal rejected its arguments (rc={rc})")
+    return trace[:, :len(rec)]
+
+
 def run_problem(p, nt=None, dtype=np.float32, kind="untiled", ftz=True, **kw):
     """Convenience: run a workloads.Problem from its generated inputs; returns (P, C, trace)
     as interior arrays."""
@@ -207,6 +237,16 @@ def run_problem(p, nt=None, dtype=np.float32, kind="untiled", ftz=True, **kw):
         dmp = embed(W.damp(p), p.ndim, r, dtype)
         a, c = medium(vel, dmp, p.dt, dtype=dtype, ftz=ftz)
     wv = W.wavelet(p, nt).astype(dtype) if p.src else None
+    if kind == "literal":
+        assert p.time_order == 2
+        vel = embed(W.velocity(p), p.ndim, r, dtype)
+        vel[vel == 0] = 1.0
+        dmp = embed(W.damp(p), p.ndim, r, dtype)
+        del a, c
+        h = p.dx[:p.ndim] if p.ndim == 3 else p.dx[:2]
+        tr = run_literal(p.ndim, p.n, p.space_order, fd_weights(p.space_order), h, p.dt, P, C, vel, dmp,
+                         nt, 0, list(p.src), wv, list(p.rec), ftz)
+        return extract(P, p.ndim, p.n, r), extract(C, p.ndim, p.n, r), tr
     fn = run_untiled if kind == "untiled" else run_skewed
     tr = fn(p.ndim, p.n, p.space_order, fd_weights(p.space_order), p.dx[:p.ndim] if p.ndim == 3 else p.dx[:2],
             p.time_order, p.dt, P, C, a, c, nt, 0, list(p.src), wv, list(p.rec), ftz, **kw)

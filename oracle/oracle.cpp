@@ -23,6 +23,10 @@
 //                      update(point).  This is "the plain definition" (SURVEY
 //                      §8(c) O1): time tiling must reproduce it exactly.
 //
+//  * O1-literal oracle_run_literal_*  the same loop nest with the paper's printed update
+//                      expression and term order, fp32: bounds the drift of the
+//                      canonical order against the paper's own (reading Q8); not the reference.
+//
 //  * O2 oracle_run_skewed_*    the paper's time-tiled schedule:
 //                      loop order tt, zz, yy, t, z', y', x with the tiled
 //                      (slow) axes skewed by `skew`*t (P:1196-1202, P:1445
@@ -190,6 +194,81 @@ int run_untiled(int ndim, long nx, long ny, long nz, int r, const double* coeffs
   return 0;
 }
 
+// ---------------------------------------------------------------------------- O1-literal
+// The paper's own expression for the damped wave update, term by term in the order printed at
+// P:1678-1708 (fp32, C left-to-right evaluation, no contraction):
+//     num = (tcse0 - 2m) u^{n-1}
+//           + w_r S_r + w_{r-1} S_{r-1} + ... + w_1 S_1      (paper: "- 8.25e-5F*(...) + ..."),
+//           + 4 m u^n  + w_0 u^n,            u^{n+1} = num / (tcse0 + 2m)
+// with tcse0 = dt*damp, m = 1/v^2, w_k = (T)(2 dt^2 c_k / h^2), w_0 = (T)(2 dt^2 ndim c_0 / h^2)
+// and S_k = u[c-k] + u[c+k] (contiguous axis) + u[y-k] + u[y+k] + u[slow-k] + u[slow+k], summed
+// left to right (the paper's contiguous axis is its z: its "z - 4" pair comes first).
+// A source term (none in the paper) enters the numerator as + (T)(2 dt^2) * w_s
+// after the neighbour sums.  Isotropic spacing only (the printed form has one weight per k).
+// This is a second, independently ordered evaluation used to bound the fp32 drift between the
+// canonical order and the paper's order (reading Q8); it is not the parity reference.
+template <class T>
+int run_literal(int ndim, long nx, long ny, long nz, int r, const double* coeffs, const double* h,
+                double dt, T* P, T* C, const T* vel, const T* damp, int nt, long step0,
+                int nsrc, const int64_t* src_xyz, const T* wavelet, int nrec, const int64_t* rec_xyz,
+                T* trace, int ftz) {
+  if (ndim != 2 && ndim != 3) return 1;
+  if (r < 1 || r > 16 || nt < 0) return 1;
+  for (int a = 1; a < ndim; ++a) if (h[a] != h[0]) return 2;
+  Geo g(ndim, nx, ny, nz, r);
+  const double s2 = 2.0 * dt * dt / (h[0] * h[0]);
+  T w[17];
+  for (int k = 1; k <= r; ++k) w[k] = (T)(s2 * coeffs[k]);
+  const T w0 = (T)(s2 * ndim * coeffs[0]);
+  const T dtT = (T)dt, two_dt2 = (T)(2.0 * dt * dt);
+  const PointList S = make_points(g, nsrc, src_xyz);
+  const PointList Rc = make_points(g, nrec, rec_xyz);
+  T* bufP = P;
+  T* bufC = C;
+  const long nzl = (ndim == 3) ? nz : 1;
+  for (int n = 0; n < nt; ++n) {
+    const T* w_step = nsrc ? wavelet + (step0 + n) * nsrc : nullptr;
+    T* N = bufP;
+    const T* Cc = bufC;
+#pragma omp parallel
+    {
+      FtzGuard guard(ftz);
+#pragma omp for schedule(static)
+      for (long z = 0; z < nzl; ++z)
+        for (long y = 0; y < ny; ++y) {
+          const bool hs = nsrc && row_has_source<T>(S, y, z);
+          for (long x = 0; x < nx; ++x) {
+            const long p = g.idx(x, y, z);
+            const T v = vel[p];
+            const T m = (T)1 / (v * v);
+            const T tcse0 = dtT * damp[p];
+            T num = (tcse0 - (T)2 * m) * N[p];       // N[p] still holds u^{n-1}
+            for (int k = r; k >= 1; --k) {
+              T sk = Cc[p - k] + Cc[p + k];
+              sk = sk + Cc[p - k * g.sy];
+              sk = sk + Cc[p + k * g.sy];
+              if (ndim == 3) { sk = sk + Cc[p - k * g.sz]; sk = sk + Cc[p + k * g.sz]; }
+              num = num + w[k] * sk;
+            }
+            if (hs)
+              for (size_t s = 0; s < S.p.size(); ++s)
+                if (S.p[s] == p) num = num + two_dt2 * w_step[s];
+            num = num + (T)4 * m * Cc[p];
+            num = num + w0 * Cc[p];
+            N[p] = num / (tcse0 + (T)2 * m);
+          }
+        }
+    }
+    for (int k = 0; k < nrec; ++k) trace[(long)n * nrec + k] = N[Rc.p[k]];
+    std::swap(bufP, bufC);
+  }
+  if (nt % 2 == 1) {
+    const long tot = g.total();
+    for (long i = 0; i < tot; ++i) std::swap(P[i], C[i]);
+  }
+  return 0;
+}
+
 // ---------------------------------------------------------------------------- O2
 // Paper's skewed, time-tiled schedule.  Tiled axes are the slow ones
 // (z and y in 3-D; y in 2-D), skewed by `skew` per time step; x (contiguous) whole.
@@ -294,6 +373,24 @@ int oracle_run_untiled_f64(int ndim, long nx, long ny, long nz, int r, const dou
                            const int64_t* rec_xyz, double* trace, int ftz) {
   return run_untiled<double>(ndim, nx, ny, nz, r, coeffs, h, time_order, dt, P, C, a, c, nt, step0,
                              nsrc, src_xyz, wavelet, nrec, rec_xyz, trace, ftz);
+}
+
+int oracle_run_literal_f32(int ndim, long nx, long ny, long nz, int r, const double* coeffs,
+                           const double* h, double dt, float* P, float* C, const float* vel,
+                           const float* damp, int nt, long step0, int nsrc, const int64_t* src_xyz,
+                           const float* wavelet, int nrec, const int64_t* rec_xyz, float* trace,
+                           int ftz) {
+  return run_literal<float>(ndim, nx, ny, nz, r, coeffs, h, dt, P, C, vel, damp, nt, step0, nsrc,
+                            src_xyz, wavelet, nrec, rec_xyz, trace, ftz);
+}
+
+int oracle_run_literal_f64(int ndim, long nx, long ny, long nz, int r, const double* coeffs,
+                           const double* h, double dt, double* P, double* C, const double* vel,
+                           const double* damp, int nt, long step0, int nsrc, const int64_t* src_xyz,
+                           const double* wavelet, int nrec, const int64_t* rec_xyz, double* trace,
+                           int ftz) {
+  return run_literal<double>(ndim, nx, ny, nz, r, coeffs, h, dt, P, C, vel, damp, nt, step0, nsrc,
+                             src_xyz, wavelet, nrec, rec_xyz, trace, ftz);
 }
 
 int oracle_run_skewed_f32(int ndim, long nx, long ny, long nz, int r, const double* coeffs,

@@ -17,6 +17,7 @@
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -55,6 +56,11 @@ struct stencil_plan {
   float dtf = 0.f;
   // scratch
   Buf ac, p2, c2, tables;
+  // exchange-tiled passes (sweept.cuh): tile table and u32 words [ticket, fault, prog[ntiles]]
+  Buf xtiles, xwords, xtrace;
+  std::vector<st::TileDesc> xt;        // host copy of the uploaded table
+  int xt_lo = -1, xt_hi = -1;          // output plane range the table was built for
+  unsigned x_ticket_base = 0, x_seq = 0;
   Buf staging;       // pinned host staging for the src/rec tables
   bool last_swapped = false;           // ST_NO_SWAP: the last run returned the pair swapped
   // fused halo push (stencil_set_peer)
@@ -241,6 +247,19 @@ struct Tables {
 extern "C" {
 
 int32_t stencil_abi_version(void) { return 104; }
+
+#ifdef ST_XTRACE
+// diagnostic builds only: copy the event trace of the last exchange pass and its tile table
+int64_t stencil_xtrace(stencil_plan* p, void* host, int64_t bytes, void* tiles_host, int64_t tiles_bytes) {
+  if (!p || !p->xtrace.ptr) return -1;
+  cudaStreamSynchronize(p->stream);
+  const size_t n = std::min<size_t>((size_t)bytes, p->xtrace.bytes);
+  cudaMemcpy(host, p->xtrace.ptr, n, cudaMemcpyDeviceToHost);
+  const size_t tn = std::min<size_t>((size_t)tiles_bytes, p->xt.size() * sizeof(st::TileDesc));
+  memcpy(tiles_host, p->xt.data(), tn);
+  return (int64_t)p->xt.size();
+}
+#endif
 
 int32_t stencil_swapped(const stencil_plan* p) { return p ? (p->last_swapped ? 1 : 0) : -1; }
 
@@ -445,6 +464,7 @@ void stencil_destroy(stencil_plan* p) {
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   for (void* h : p->ipc_opened) cudaIpcCloseMemHandle(h);
   free_buf(p->counters);
+  free_buf(p->xtiles); free_buf(p->xwords); free_buf(p->xtrace);
   delete p;
 }
 
@@ -482,6 +502,15 @@ st_status stencil_sync(stencil_plan* p) {
   cudaSetDevice(p->device);
   cudaError_t e = cudaStreamSynchronize(p->stream);
   if (e != cudaSuccess) { p->broken = true; return cuda_fail(p, e, "stream synchronize"); }
+  if (p->xwords.ptr) {   // an exchange-tiled pass whose neighbour wait timed out (sweept.cuh)
+    unsigned fault = 0;
+    e = cudaMemcpy(&fault, static_cast<unsigned*>(p->xwords.ptr) + 1, sizeof fault, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) { p->broken = true; return cuda_fail(p, e, "fault word read"); }
+    if (fault) {
+      p->broken = true;
+      return fail(p, ST_ECUDA, "exchange-tiled pass: a tile's wait for its neighbours timed out (results invalid)");
+    }
+  }
   return ST_OK;
 }
 
@@ -569,6 +598,89 @@ static int choose_chunks(const stencil_plan* p, const st::KernelEntry* k, int bp
   return bestc;
 }
 
+// ------------------------------------------------------------------ exchange-tiled pass plan
+// Tiles of one T_k = 2 exchange pass (sweept.cuh header): 64 x H tiles in bands of at most
+// `slots / tiles_x` tile rows (a band must be resident at once), z-chunks as independent copies.
+// Band cut: band b+1's first tile row starts r rows above the end of band b's level-1 rows, band
+// b's last tile row produces level 2 for H - r rows.  Returns the chunk count chosen.
+static int plan_tiles(const stencil_plan* p, const st::KernelEntry* k, int out_lo, int out_hi,
+                      int slots, std::vector<st::TileDesc>& T) {
+  const int H = k->oy, r = k->radius;
+  const int nx = (int)p->nx, ny = (int)p->ny;
+  const int tx = (nx + 63) / 64;
+  // test/tuning overrides: ST_EXCH_SLOTS caps the resident tiles a band may use (forces band
+  // cuts on small grids), ST_EXCH_CHUNKS fixes the z-chunk count
+  if (const char* e = getenv("ST_EXCH_SLOTS")) slots = std::max(1, std::min(slots, atoi(e)));
+  int force_c = 0;
+  if (const char* e = getenv("ST_EXCH_CHUNKS")) force_c = std::max(1, atoi(e));
+  const int mmax = std::max(1, slots / tx);
+  struct Row { int y0, l2_lo, l2_hi; bool first, last; };   // tile rows, band-major
+  std::vector<Row> rows;
+  std::vector<int> band_of;
+  int L = 0, b = 0;
+  while (L < ny) {
+    const int m_need = (ny - L + H - 1) / H;
+    const bool last_band = m_need <= mmax;
+    const int m = last_band ? m_need : mmax;
+    for (int i = 0; i < m; ++i) {
+      Row w;
+      w.y0 = L + i * H;
+      w.l2_lo = w.y0;
+      w.l2_hi = (i == m - 1) ? (last_band ? std::min(w.y0 + H, ny) : w.y0 + H - r) : w.y0 + H;
+      w.first = (i == 0);
+      w.last = (i == m - 1);
+      rows.push_back(w);
+      band_of.push_back(b);
+    }
+    if (last_band) break;
+    L = L + m * H - r;
+    ++b;
+  }
+  const int nrow = (int)rows.size();
+  const long long planes = out_hi - out_lo;
+  // chunk count: whole waves of `slots` tiles x (chunk planes + the 4r-plane warm-up)
+  int best_c = 1;
+  double best_t = 1e300;
+  for (int c = 1; c <= 32; ++c) {
+    const long long chunk = (planes + c - 1) / c;
+    if (c > 1 && chunk < std::max(8, 2 * r)) break;
+    const long long ntile = (long long)c * nrow * tx;
+    const double t = (double)((ntile + slots - 1) / slots) * (double)(chunk + 4 * r);
+    if (t < best_t * 0.999) { best_t = t; best_c = c; }
+  }
+  if (force_c) best_c = (int)std::min<long long>(force_c, std::max<long long>(1, planes));
+  const int zc = (int)((planes + best_c - 1) / best_c);
+  T.clear();
+  for (int c = 0; c < best_c; ++c) {
+    const int zb = out_lo + c * zc, ze = std::min(out_hi, zb + zc);
+    if (zb >= ze) break;
+    const int base = (int)T.size();
+    for (int j = 0; j < nrow; ++j) {
+      for (int i = 0; i < tx; ++i) {
+        st::TileDesc d{};
+        d.x0 = 64 * i;
+        d.y0 = rows[j].y0;
+        d.l2_lo = rows[j].l2_lo;
+        d.l2_hi = rows[j].l2_hi;
+        d.st_lo = rows[j].y0;
+        d.st_hi = std::min(rows[j].y0 + H, ny);
+        d.zb = zb;
+        d.ze = ze;
+        const int me = base + j * tx + i;
+        // above: previous tile row (same band, or the band above's last row)
+        d.dep[0] = (j > 0) ? me - tx : -1;
+        // below: next tile row of the same band, unless this row stops its level 2 at H - r
+        d.dep[1] = (!rows[j].last) ? me + tx : -1;
+        d.dep[2] = (i > 0) ? me - 1 : -1;
+        d.dep[3] = (i < tx - 1) ? me + 1 : -1;
+        T.push_back(d);
+      }
+    }
+  }
+  (void)band_of;
+  return best_c;
+}
+
 static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
                           const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
                           const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
@@ -633,8 +745,9 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   // buffers: 0 = caller P, 1 = caller C, 2 = scratch P2, 3 = scratch C2
   float* bufs[4] = {u_prev, u_cur, static_cast<float*>(p->p2.ptr), static_cast<float*>(p->c2.ptr)};
   int prev = 0, cur = 1;
-  CUtensorMap maps_t1[4], maps_tk[4], maps_p0[4], maps_u1[4], map_a0, map_a1;
+  CUtensorMap maps_t1[4], maps_tk[4], maps_p0[4], maps_u1[4], maps_l1[4], map_a0, map_a1;
   bool have_t1[4] = {false, false, false, false}, have_tk[4] = {false, false, false, false};
+  bool have_l1[4] = {false, false, false, false};
   bool have_p0[4] = {false, false, false, false}, have_u1[4] = {false, false, false, false};
   bool have_ac = false;
   st::KernelMaps km{};
@@ -644,6 +757,7 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   sp.gz_lo = p->has_lo ? 0 : (int)p->G;
   sp.gz_hi = p->has_hi ? (int)p->Z : (int)(p->G + p->nzl);
   sp.zv_lo = (int)zv_lo;
+  sp.zv_hi = (int)zv_hi;
   sp.ac = static_cast<const float4*>(p->ac.ptr);
   sp.K0 = p->K0; sp.dt = p->dtf;
   memcpy(sp.W, p->W, sizeof sp.W);
@@ -734,6 +848,56 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
     const int chunks = choose_chunks(p, k, bps, tiles, planes);
     sp.zchunk = (int)((planes + chunks - 1) / chunks);
     dim3 grid((unsigned)((p->nx + k->ox - 1) / k->ox), (unsigned)((p->ny + k->oy - 1) / k->oy), (unsigned)chunks);
+    sp.x_tiles = nullptr; sp.x_ntiles = 0; sp.x_ticket = sp.x_prog = sp.x_fault = nullptr;
+    sp.x_trace = nullptr;
+    if (k->exch) {
+      // exchange-tiled pass: tile table (rebuilt when the output plane range changes), ticket,
+      // progress words; level-1 box map over this pass's u^{n+1} output field
+      if (p->xt_lo != sp.out_lo || p->xt_hi != sp.out_hi) {
+        plan_tiles(p, k, sp.out_lo, sp.out_hi, p->sm_count * std::max(1, bps), p->xt);
+        const size_t tb = p->xt.size() * sizeof(st::TileDesc);
+        s = ensure_buf(p, p->xtiles, tb, "tile table");
+        if (s != ST_OK) return s;
+        CK(cudaMemcpyAsync(p->xtiles.ptr, p->xt.data(), tb, cudaMemcpyHostToDevice, p->stream), "tile table upload");
+        const size_t wb = (2 + p->xt.size()) * sizeof(unsigned);
+        if (p->xwords.bytes < wb) {
+          s = ensure_buf(p, p->xwords, wb, "exchange words");
+          if (s != ST_OK) return s;
+          CK(cudaMemsetAsync(p->xwords.ptr, 0, wb, p->stream), "exchange words reset");
+          p->x_ticket_base = 0;
+          p->x_seq = 1;
+        }
+        p->xt_lo = sp.out_lo; p->xt_hi = sp.out_hi;
+      }
+      const int op = (sp.outP == bufs[0]) ? 0 : (sp.outP == bufs[1]) ? 1 : (sp.outP == bufs[2]) ? 2 : 3;
+      if (!have_l1[op]) {
+        s = encode_map(p, k, bufs[op], &maps_l1[op]);
+        if (s != ST_OK) return s;
+        have_l1[op] = true;
+      }
+      km.u1 = maps_l1[op];
+      unsigned* w = static_cast<unsigned*>(p->xwords.ptr);
+      sp.x_tiles = static_cast<const st::TileDesc*>(p->xtiles.ptr);
+      sp.x_ntiles = (int)p->xt.size();
+      sp.x_ticket = w;
+      sp.x_fault = w + 1;
+      sp.x_prog = w + 2;
+      sp.x_ticket_base = p->x_ticket_base;
+      sp.x_prog_base = p->x_seq << 16;
+      sp.x_trace = nullptr;
+#ifdef ST_XTRACE
+      {
+        const size_t tb = p->xt.size() * (size_t)ST_XTRACE_K * 12 * 8;
+        s = ensure_buf(p, p->xtrace, tb, "trace");
+        if (s != ST_OK) return s;
+        CK(cudaMemsetAsync(p->xtrace.ptr, 0, tb, p->stream), "trace reset");
+        sp.x_trace = static_cast<unsigned long long*>(p->xtrace.ptr);
+      }
+#endif
+      p->x_ticket_base += (unsigned)p->xt.size();
+      ++p->x_seq;
+      grid = dim3((unsigned)p->xt.size(), 1, 1);
+    }
     sp.push_lo = sp.push_hi = nullptr;
     sp.band_lo = INT_MIN; sp.band_hi = INT_MAX;
     sp.sig_lo = sp.sig_hi = nullptr;

@@ -9,6 +9,7 @@
 #include "sweep1.cuh"
 #include "sweep1s.cuh"
 #include "sweep2.cuh"
+#include "sweept.cuh"
 
 #ifndef ST_T1_DEPTH
 #define ST_T1_DEPTH 6   // untiled kernel: ring planes of prefetch beyond the radius+1 in use
@@ -35,6 +36,8 @@ struct KernelEntry {
   int ebw = 0, eh0 = 0, eh1 = 0;   // time-tiled kernel (wave): field box width, level-0 / level-1
                                    // box rows of the producer-streamed u^{n-1}, u^n, medium
   int fixed_slots = 0;             // > 0: the ring depth is compiled in (sweep1s_kernel)
+  int exch = 0;                    // 1: exchange-tiled kernel (sweept.cuh): host builds a tile
+                                   //    table; maps.u1 = level-1 box over the output field
 };
 
 // Defined in the generated instance translation units.
@@ -230,6 +233,38 @@ constexpr KernelEntry make_entry2() {
                      R, (size_t)G::SLOT_BYTES, (size_t)G::FIXED_BYTES,
                      &launch_sweep2<R, TK, WAVE, OY>, &query_sweep2<R, TK, WAVE, OY>, ST_T2_DEPTH,
                      WAVE ? G::EBW : 0, WAVE ? G::GH : 0, WAVE ? G::OY : 0};
+}
+
+// ---- exchange-tiled kernel (sweept.cuh): T_k = 2, level-1 halo read back through L2
+template <int R, bool WAVE, int NCW, int VY, int D>
+cudaError_t launch_sweept(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
+                          size_t smem, cudaStream_t stream) {
+  (void)nslot;
+  return launch_pdl(sweept_kernel<R, WAVE, NCW, VY, D>, grid, 32 * (NCW + 3), smem, stream, maps.u, maps.u1, p);
+}
+
+template <int R, bool WAVE, int NCW, int VY, int D>
+cudaError_t query_sweept(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweept_kernel<R, WAVE, NCW, VY, D>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (attr) {
+    e = cudaFuncGetAttributes(attr, k);
+    if (e != cudaSuccess) return e;
+  }
+  if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, nthreads, smem);
+  return cudaSuccess;
+}
+
+template <int R, bool WAVE, int NCW, int VY, int D>
+constexpr KernelEntry make_entryT() {
+  using G = GeomT<R, NCW, VY, WAVE, D>;
+  KernelEntry e{3, WAVE ? 2 : 1, R, 2, VY, NCW, G::NTHREADS, 64, G::H, G::BW, G::BH,
+                R, (size_t)G::SLOT_BYTES, (size_t)(G::SMEM - G::NU * G::SLOT_BYTES),
+                &launch_sweept<R, WAVE, NCW, VY, D>, &query_sweept<R, WAVE, NCW, VY, D>, 0};
+  e.fixed_slots = G::NU;
+  e.exch = 1;
+  return e;
 }
 
 }  // namespace st

@@ -25,12 +25,21 @@ namespace st {
 
 constexpr int kMaxR = 8;
 
+// One tile of the exchange-tiled pass (sweept.cuh; built by abi.cu plan_tiles).
+struct TileDesc {
+  int x0, y0;             // level-1 region: columns [x0, x0+64), rows [y0, y0+H) (interior coords)
+  int l2_lo, l2_hi;       // rows whose level 2 (u^{n+2}) this tile produces
+  int st_lo, st_hi;       // rows whose level 1 (u^{n+1}) this tile stores
+  int zb, ze;             // level-2 output planes (array coordinates)
+  int dep[4];             // tiles whose stored level 1 feeds this tile's level-2 halo (-1: none)
+};
+
 struct SweepParams {
   int nx, ny;                 // interior extents (x, y)
   int X;                      // row pitch in floats (multiple of 32)
   long long plane;            // X * Y floats per plane
   int gz_lo, gz_hi;           // array planes inside the GLOBAL interior [gz_lo, gz_hi)
-  int zv_lo;                  // array plane of TMA z-coordinate 0
+  int zv_lo, zv_hi;           // array planes covered by the tensor maps [zv_lo, zv_hi)
   int out_lo, out_hi;         // planes this pass must produce (last level)
   int zchunk;                 // output planes per CTA (gridDim.z chunks)
   const float* P;             // u^{n-1}
@@ -72,6 +81,16 @@ struct SweepParams {
   const unsigned long long* wait_hi;
   unsigned long long wait_lo_target, wait_hi_target;
   int iso;                    // W[0][k] == W[1][k] == W[2][k] bitwise for every k (isotropic dx)
+  // exchange-tiled pass (sweept.cuh): tile table, ticket counter, per-tile level-1 progress
+  // (values base + planes done, compared modulo 2^32), fault word of timed-out waits
+  const TileDesc* x_tiles;
+  int x_ntiles;
+  unsigned* x_ticket;
+  unsigned x_ticket_base;
+  unsigned* x_prog;
+  unsigned x_prog_base;
+  unsigned* x_fault;
+  unsigned long long* x_trace;   // ST_XTRACE builds only: per (tile, plane) event timestamps
 };
 
 // Tensor maps of one launch: u = u^n box with halo (every kernel); the time-tiled kernel's
