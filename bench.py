@@ -276,10 +276,10 @@ def _kernel_name(p: W.Problem, tk: int) -> str:
     """Name of the compiled sweep instance a pass of this problem launches (build.instances())."""
     from paper_1707_02347_b200.build import instances
     names = {0: "st::sweep_kernel", 1: "st::sweep1_kernel", 2: "st::sweep2_kernel", 3: "st::sweep1s_kernel",
-             4: "st::sweept_kernel"}
+             4: "st::sweepx_kernel"}
     for (ndim, wave, R, TK, VY, NWY, kind) in instances():
         if (ndim, wave, R, TK) == (p.ndim, int(p.time_order == 2), p.radius, tk):
-            return f"{names[kind]}<R={R}, T_k={TK}>"
+            return f"{names.get(kind, f'kind{kind}')}<R={R}, T_k={TK}>"
     return "st::sweep_kernel"
 
 

@@ -46,7 +46,7 @@ def _t1_geom(ndim: int, wave: int, R: int):
 
 # kernel kinds: 1 = sweep1 (untiled, warp-specialised), 3 = sweep1s (untiled, static 2r+1 ring),
 #               2 = sweep2 (time-tiled, warp-specialised, overlapped tiles),
-#               4 = sweept (time-tiled T_k = 2, level-1 halo exchanged through L2),
+#               4 = sweepx (time-tiled T_k = 2 as L1/L2 untiled sweeps chained through L2),
 #               0 = sweep (first time-tiled kernel; 2-D and the shapes sweep2 does not fit)
 def _sweep2_oy(wave: int, R: int, TK: int):
     """Output rows of the sweep2 (one warp group per level) instance, or None if it does not fit
@@ -73,31 +73,10 @@ def _static_ring(ndim: int, wave: int, R: int) -> bool:
     return ndim == 3 and R in (5, 6, 8)
 
 
-def _exch_fits(wave: int, R: int, ncw: int = 16, vy: int = 1, d: int = 0) -> bool:
-    """GeomT<R, NCW, VY, WAVE, D>::OK (sweept.cuh): the exchange-tiled kernel's rings fit in 227 KB."""
-    H = ncw * vy
-    if H < 2 * R:
-        return False
-    rxb = (R + 3) & ~3
-    slot = ((64 + 2 * rxb) * (H + 2 * R) * 4 + 127) // 128 * 128
-    pd = 3
-    stage = ncw * ((pd + 1) * vy * 64 + (pd + 1 + R + d) * vy * 128) * 4 if wave else 0
-    nb = min(R + d + 1, 6)
-    fixed = 1024 + stage + nb * slot
-    nu = min((227 * 1024 - fixed) // slot, R + 5)
-    return nu >= R + 2
-
-
-EXCH_OVERRIDE = {}   # R -> (ncw, vy, d): experiment builds (build_variant(exch=...))
-
-
-def _exch_geom(R: int):
-    """(consumer warps, rows per warp, level-2 lag D) of the exchange-tiled kernel.  Registers are
-    allocated per SM sub-partition: 16 warps (4 per SMSP) leave 128 per thread, 18 warps only 96,
-    9 warps 168; the two z-queues hold 2 x (2r+1+D) x VY packed pairs per thread."""
-    if R in EXCH_OVERRIDE:
-        return EXCH_OVERRIDE[R]
-    return (13, 1, 2) if R <= 5 else (13, 1, 1) if R == 6 else (6, 2, 1)
+def _exch(wave: int, R: int) -> bool:
+    """T_k = 2 instances built as the two-role exchange pass (sweepx.cuh): wave r >= 3 (measured
+    faster than the overlapped-tile sweep2 at SO8 and SO12) and heat r <= 2."""
+    return (wave and R >= 3) or (not wave and R <= 2)
 
 
 def instances():
@@ -109,9 +88,8 @@ def instances():
             ncw, vy = _t1_geom(3, wave, R)
             out.append((3, wave, R, 1, vy, ncw, 3 if _static_ring(3, wave, R) else 1))
             oy = _sweep2_oy(wave, R, 2)
-            eg = _exch_geom(R)
-            if (wave or R <= 2) and _exch_fits(wave, R, *eg):
-                out.append((3, wave, R, 2, eg[1], eg[0], 4))   # D: _exch_geom(R)[2]
+            if _exch(wave, R):
+                out.append((3, wave, R, 2, vy, ncw, 4))        # L1/L2 roles, untiled geometry
             elif oy:
                 out.append((3, wave, R, 2, 2, oy, 2))
             else:
@@ -144,7 +122,7 @@ def _gen_sources(groups: int, inst=None, outdir: str = BUILD):
             elif kind == 2:
                 lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}>(),")   # NWY = output rows
             elif kind == 4:
-                lines.append(f"  make_entryT<{R}, {w}, {NWY}, {VY}, {_exch_geom(R)[2]}>(),")
+                lines.append(f"  make_entryX<{R}, {w}, {NWY}, {VY}>(),")
             else:
                 lines.append(f"  make_entry<{R}, {TK}, {w}, {ndim}, {VY}, {NWY}>(),")
         lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]
@@ -185,7 +163,7 @@ def _compile(src: str, outdir: str = BUILD, defines=()):
     obj = os.path.join(outdir, os.path.basename(src) + ".o")
     deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "sweep1.cuh"),
             os.path.join(CSRC, "sweep2.cuh"), os.path.join(CSRC, "sweep1s.cuh"),
-            os.path.join(CSRC, "sweept.cuh"),
+            os.path.join(CSRC, "sweepx.cuh"),
             os.path.join(CSRC, "registry.h"),
             os.path.join(HERE, "..", "include", "stencil.h")]
     stamp = obj + ".stamp"
@@ -230,12 +208,9 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
 
 
 def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = True,
-                  static_r=None, oy2=None, exch=None) -> str:
+                  static_r=None, oy2=None) -> str:
     """Experimental library _variants/libstencil_<name>.so with extra -D flags and (optionally)
     only the instances whose (ndim, wave, R, TK) is listed; load it with ST_LIB=<path>."""
-    EXCH_OVERRIDE.clear()
-    if exch:
-        EXCH_OVERRIDE.update(exch)   # {R: (ncw, vy, d)} for the exchange-tiled instances
     inst = instances()
     if only is not None:
         inst = [i for i in inst if tuple(i[:4]) in set(map(tuple, only))]
@@ -249,10 +224,7 @@ def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = Tru
                 else i for i in inst]
     if t1 is not None:   # (consumer warps, rows per warp) of the untiled kernel
         inst = [i[:4] + (t1[1], t1[0], i[6]) if i[6] in (1, 3) else i for i in inst]
-    try:
-        return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose)
-    finally:
-        EXCH_OVERRIDE.clear()
+    return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose)
 
 
 if __name__ == "__main__":

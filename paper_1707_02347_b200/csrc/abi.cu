@@ -56,10 +56,11 @@ struct stencil_plan {
   float dtf = 0.f;
   // scratch
   Buf ac, p2, c2, tables;
-  // exchange-tiled passes (sweept.cuh): tile table and u32 words [ticket, fault, prog[ntiles]]
+  // two-role exchange passes (sweepx.cuh): tile table and u32 words [ticket, fault, prog[ntiles]]
   Buf xtiles, xwords, xtrace;
-  std::vector<st::TileDesc> xt;        // host copy of the uploaded table
+  std::vector<st::XTile> xx;           // host copy of the uploaded tile table
   int xt_lo = -1, xt_hi = -1;          // output plane range the table was built for
+  int x_ntiles = 0;                    // tiles of that table
   unsigned x_ticket_base = 0, x_seq = 0;
   Buf staging;       // pinned host staging for the src/rec tables
   bool last_swapped = false;           // ST_NO_SWAP: the last run returned the pair swapped
@@ -255,9 +256,9 @@ int64_t stencil_xtrace(stencil_plan* p, void* host, int64_t bytes, void* tiles_h
   cudaStreamSynchronize(p->stream);
   const size_t n = std::min<size_t>((size_t)bytes, p->xtrace.bytes);
   cudaMemcpy(host, p->xtrace.ptr, n, cudaMemcpyDeviceToHost);
-  const size_t tn = std::min<size_t>((size_t)tiles_bytes, p->xt.size() * sizeof(st::TileDesc));
-  memcpy(tiles_host, p->xt.data(), tn);
-  return (int64_t)p->xt.size();
+  const size_t tn = std::min<size_t>((size_t)tiles_bytes, p->xx.size() * sizeof(st::XTile));
+  memcpy(tiles_host, p->xx.data(), tn);
+  return (int64_t)p->xx.size();
 }
 #endif
 
@@ -502,13 +503,13 @@ st_status stencil_sync(stencil_plan* p) {
   cudaSetDevice(p->device);
   cudaError_t e = cudaStreamSynchronize(p->stream);
   if (e != cudaSuccess) { p->broken = true; return cuda_fail(p, e, "stream synchronize"); }
-  if (p->xwords.ptr) {   // an exchange-tiled pass whose neighbour wait timed out (sweept.cuh)
+  if (p->xwords.ptr) {   // an exchange pass whose wait timed out (sweepx.cuh)
     unsigned fault = 0;
     e = cudaMemcpy(&fault, static_cast<unsigned*>(p->xwords.ptr) + 1, sizeof fault, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) { p->broken = true; return cuda_fail(p, e, "fault word read"); }
     if (fault) {
       p->broken = true;
-      return fail(p, ST_ECUDA, "exchange-tiled pass: a tile's wait for its neighbours timed out (results invalid)");
+      return fail(p, ST_ECUDA, "exchange pass: a tile's wait for the tiles it depends on timed out (results invalid)");
     }
   }
   return ST_OK;
@@ -598,87 +599,78 @@ static int choose_chunks(const stencil_plan* p, const st::KernelEntry* k, int bp
   return bestc;
 }
 
-// ------------------------------------------------------------------ exchange-tiled pass plan
-// Tiles of one T_k = 2 exchange pass (sweept.cuh header): 64 x H tiles in bands of at most
-// `slots / tiles_x` tile rows (a band must be resident at once), z-chunks as independent copies.
-// Band cut: band b+1's first tile row starts r rows above the end of band b's level-1 rows, band
-// b's last tile row produces level 2 for H - r rows.  Returns the chunk count chosen.
-static int plan_tiles(const stencil_plan* p, const st::KernelEntry* k, int out_lo, int out_hi,
-                      int slots, std::vector<st::TileDesc>& T) {
+// ------------------------------------------------------------------ two-role exchange pass plan
+// Tiles of one sweepx pass (sweepx.cuh header): L1 tiles on the regular 64 x H grid, L2 tiles on
+// the same grid shifted r rows up, in the ticket order L1 row 0, L2 row 0, L1 row 1, ... per
+// z-chunk; an L2 tile waits on the L1 tiles of its own and the previous row and the x-neighbours.
+static void plan_xtiles(const stencil_plan* p, const st::KernelEntry* k, int out_lo, int out_hi,
+                        int slots, std::vector<st::XTile>& T) {
   const int H = k->oy, r = k->radius;
   const int nx = (int)p->nx, ny = (int)p->ny;
   const int tx = (nx + 63) / 64;
-  // test/tuning overrides: ST_EXCH_SLOTS caps the resident tiles a band may use (forces band
-  // cuts on small grids), ST_EXCH_CHUNKS fixes the z-chunk count
-  if (const char* e = getenv("ST_EXCH_SLOTS")) slots = std::max(1, std::min(slots, atoi(e)));
-  int force_c = 0;
-  if (const char* e = getenv("ST_EXCH_CHUNKS")) force_c = std::max(1, atoi(e));
-  const int mmax = std::max(1, slots / tx);
-  struct Row { int y0, l2_lo, l2_hi; bool first, last; };   // tile rows, band-major
-  std::vector<Row> rows;
-  std::vector<int> band_of;
-  int L = 0, b = 0;
-  while (L < ny) {
-    const int m_need = (ny - L + H - 1) / H;
-    const bool last_band = m_need <= mmax;
-    const int m = last_band ? m_need : mmax;
-    for (int i = 0; i < m; ++i) {
-      Row w;
-      w.y0 = L + i * H;
-      w.l2_lo = w.y0;
-      w.l2_hi = (i == m - 1) ? (last_band ? std::min(w.y0 + H, ny) : w.y0 + H - r) : w.y0 + H;
-      w.first = (i == 0);
-      w.last = (i == m - 1);
-      rows.push_back(w);
-      band_of.push_back(b);
-    }
-    if (last_band) break;
-    L = L + m * H - r;
-    ++b;
-  }
-  const int nrow = (int)rows.size();
+  const int rows1 = (ny + H - 1) / H;            // L1 rows [jH, jH+H)
+  const int rows2 = (ny + r + H - 1) / H;        // L2 rows [jH-r, jH+H-r)
+  const int zv_lo = (int)(p->G - (p->has_lo ? p->G : 0));
+  const int zv_hi = (int)(p->G + p->nzl + (p->has_hi ? p->G : 0));
   const long long planes = out_hi - out_lo;
-  // chunk count: whole waves of `slots` tiles x (chunk planes + the 4r-plane warm-up)
   int best_c = 1;
   double best_t = 1e300;
+  const long long per_chunk = (long long)tx * (rows1 + rows2);
   for (int c = 1; c <= 32; ++c) {
     const long long chunk = (planes + c - 1) / c;
     if (c > 1 && chunk < std::max(8, 2 * r)) break;
-    const long long ntile = (long long)c * nrow * tx;
-    const double t = (double)((ntile + slots - 1) / slots) * (double)(chunk + 4 * r);
+    const long long ntile = c * per_chunk;
+    // waves x (chunk planes + the 2r-plane warm-up + the r-plane L1 overlap on each side)
+    const double t = (double)((ntile + slots - 1) / slots) * (double)(chunk + 3 * r);
     if (t < best_t * 0.999) { best_t = t; best_c = c; }
   }
-  if (force_c) best_c = (int)std::min<long long>(force_c, std::max<long long>(1, planes));
+  if (const char* e = getenv("ST_EXCH_CHUNKS")) best_c = std::max(1, std::min<int>(atoi(e), (int)planes));
   const int zc = (int)((planes + best_c - 1) / best_c);
   T.clear();
   for (int c = 0; c < best_c; ++c) {
-    const int zb = out_lo + c * zc, ze = std::min(out_hi, zb + zc);
-    if (zb >= ze) break;
+    const int czb = out_lo + c * zc, cze = std::min(out_hi, czb + zc);
+    if (czb >= cze) break;
     const int base = (int)T.size();
-    for (int j = 0; j < nrow; ++j) {
-      for (int i = 0; i < tx; ++i) {
-        st::TileDesc d{};
-        d.x0 = 64 * i;
-        d.y0 = rows[j].y0;
-        d.l2_lo = rows[j].l2_lo;
-        d.l2_hi = rows[j].l2_hi;
-        d.st_lo = rows[j].y0;
-        d.st_hi = std::min(rows[j].y0 + H, ny);
-        d.zb = zb;
-        d.ze = ze;
-        const int me = base + j * tx + i;
-        // above: previous tile row (same band, or the band above's last row)
-        d.dep[0] = (j > 0) ? me - tx : -1;
-        // below: next tile row of the same band, unless this row stops its level 2 at H - r
-        d.dep[1] = (!rows[j].last) ? me + tx : -1;
-        d.dep[2] = (i > 0) ? me - 1 : -1;
-        d.dep[3] = (i < tx - 1) ? me + 1 : -1;
-        T.push_back(d);
+    std::vector<int> l1_index((size_t)rows1 * tx, -1);
+    std::vector<int> l2_index((size_t)rows2 * tx, -1);
+    for (int j = 0; j < std::max(rows1, rows2); ++j) {
+      if (j < rows1) {
+        for (int i = 0; i < tx; ++i) {
+          st::XTile d{};
+          d.x0 = 64 * i; d.y0 = j * H; d.role = 0;
+          d.zb = std::max(czb - r, zv_lo); d.ze = std::min(cze + r, zv_hi);
+          d.oz0 = czb; d.oz1 = cze;
+          d.nd = 0;
+          d.partner = -1;
+          for (int q = 0; q < 9; ++q) d.dep[q] = -1;
+          l1_index[(size_t)j * tx + i] = (int)T.size();
+          T.push_back(d);
+        }
+      }
+      if (j < rows2) {
+        for (int i = 0; i < tx; ++i) {
+          st::XTile d{};
+          d.x0 = 64 * i; d.y0 = j * H - r; d.role = 1;
+          d.zb = czb; d.ze = cze; d.oz0 = czb; d.oz1 = cze;
+          for (int q = 0; q < 9; ++q) d.dep[q] = -1;
+          // the u^{n+1} box covers rows [jH-2r, jH+H) and columns [64i-r, 64i+64+r)
+          const int ylo = std::max(0, j * H - 2 * r), yhi = std::min(ny, j * H + H);
+          int nd = 0;
+          if (ylo < yhi) {
+            for (int jj = ylo / H; jj <= (yhi - 1) / H && jj < rows1; ++jj)
+              for (int ii = std::max(0, i - 1); ii <= std::min(tx - 1, i + 1); ++ii)
+                if (nd < 9) d.dep[nd++] = l1_index[(size_t)jj * tx + ii];
+          }
+          d.nd = nd;
+          d.partner = -1;
+          l2_index[(size_t)j * tx + i] = (int)T.size();
+          if (j < rows1) T[(size_t)l1_index[(size_t)j * tx + i]].partner = (int)T.size();
+          T.push_back(d);
+        }
       }
     }
+    (void)base;
   }
-  (void)band_of;
-  return best_c;
 }
 
 static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
@@ -854,19 +846,22 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
       // exchange-tiled pass: tile table (rebuilt when the output plane range changes), ticket,
       // progress words; level-1 box map over this pass's u^{n+1} output field
       if (p->xt_lo != sp.out_lo || p->xt_hi != sp.out_hi) {
-        plan_tiles(p, k, sp.out_lo, sp.out_hi, p->sm_count * std::max(1, bps), p->xt);
-        const size_t tb = p->xt.size() * sizeof(st::TileDesc);
+        plan_xtiles(p, k, sp.out_lo, sp.out_hi, p->sm_count * std::max(1, bps), p->xx);
+        const size_t tb = p->xx.size() * sizeof(st::XTile), nt_ = p->xx.size();
+        const void* hsrc = p->xx.data();
+        p->x_ntiles = (int)nt_;
         s = ensure_buf(p, p->xtiles, tb, "tile table");
         if (s != ST_OK) return s;
-        CK(cudaMemcpyAsync(p->xtiles.ptr, p->xt.data(), tb, cudaMemcpyHostToDevice, p->stream), "tile table upload");
-        const size_t wb = (2 + p->xt.size()) * sizeof(unsigned);
-        if (p->xwords.bytes < wb) {
-          s = ensure_buf(p, p->xwords, wb, "exchange words");
-          if (s != ST_OK) return s;
-          CK(cudaMemsetAsync(p->xwords.ptr, 0, wb, p->stream), "exchange words reset");
-          p->x_ticket_base = 0;
-          p->x_seq = 1;
-        }
+        CK(cudaMemcpyAsync(p->xtiles.ptr, hsrc, tb, cudaMemcpyHostToDevice, p->stream), "tile table upload");
+        // a new table restarts the ticket and progress sequence (words zeroed, stream-ordered
+        // after every earlier pass): progress values are base + plane with base = seq << 16, so a
+        // word is "older than this launch" iff (int)(word - base) < 0
+        const size_t wb = (2 + nt_) * sizeof(unsigned);
+        s = ensure_buf(p, p->xwords, wb, "exchange words");
+        if (s != ST_OK) return s;
+        CK(cudaMemsetAsync(p->xwords.ptr, 0, wb, p->stream), "exchange words reset");
+        p->x_ticket_base = 0;
+        p->x_seq = 1;
         p->xt_lo = sp.out_lo; p->xt_hi = sp.out_hi;
       }
       const int op = (sp.outP == bufs[0]) ? 0 : (sp.outP == bufs[1]) ? 1 : (sp.outP == bufs[2]) ? 2 : 3;
@@ -877,8 +872,8 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
       }
       km.u1 = maps_l1[op];
       unsigned* w = static_cast<unsigned*>(p->xwords.ptr);
-      sp.x_tiles = static_cast<const st::TileDesc*>(p->xtiles.ptr);
-      sp.x_ntiles = (int)p->xt.size();
+      sp.x_tiles = p->xtiles.ptr;
+      sp.x_ntiles = p->x_ntiles;
       sp.x_ticket = w;
       sp.x_fault = w + 1;
       sp.x_prog = w + 2;
@@ -887,16 +882,20 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
       sp.x_trace = nullptr;
 #ifdef ST_XTRACE
       {
-        const size_t tb = p->xt.size() * (size_t)ST_XTRACE_K * 12 * 8;
+        const size_t tb = (size_t)p->x_ntiles * (size_t)ST_XTRACE_K * 12 * 8;
         s = ensure_buf(p, p->xtrace, tb, "trace");
         if (s != ST_OK) return s;
         CK(cudaMemsetAsync(p->xtrace.ptr, 0, tb, p->stream), "trace reset");
         sp.x_trace = static_cast<unsigned long long*>(p->xtrace.ptr);
       }
 #endif
-      p->x_ticket_base += (unsigned)p->xt.size();
-      ++p->x_seq;
-      grid = dim3((unsigned)p->xt.size(), 1, 1);
+      p->x_ticket_base += (unsigned)p->x_ntiles;
+      if (++p->x_seq == 0x8000u) {   // keep base < 2^31: restart the sequence (words zeroed)
+        CK(cudaMemsetAsync(p->xwords.ptr, 0, (2 + (size_t)p->x_ntiles) * sizeof(unsigned), p->stream), "exchange words reset");
+        p->x_ticket_base = 0;
+        p->x_seq = 1;
+      }
+      grid = dim3((unsigned)p->x_ntiles, 1, 1);
     }
     sp.push_lo = sp.push_hi = nullptr;
     sp.band_lo = INT_MIN; sp.band_hi = INT_MAX;

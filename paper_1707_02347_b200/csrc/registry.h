@@ -9,7 +9,7 @@
 #include "sweep1.cuh"
 #include "sweep1s.cuh"
 #include "sweep2.cuh"
-#include "sweept.cuh"
+#include "sweepx.cuh"
 
 #ifndef ST_T1_DEPTH
 #define ST_T1_DEPTH 6   // untiled kernel: ring planes of prefetch beyond the radius+1 in use
@@ -36,8 +36,8 @@ struct KernelEntry {
   int ebw = 0, eh0 = 0, eh1 = 0;   // time-tiled kernel (wave): field box width, level-0 / level-1
                                    // box rows of the producer-streamed u^{n-1}, u^n, medium
   int fixed_slots = 0;             // > 0: the ring depth is compiled in (sweep1s_kernel)
-  int exch = 0;                    // 1: exchange-tiled kernel (sweept.cuh): host builds a tile
-                                   //    table; maps.u1 = level-1 box over the output field
+  int exch = 0;                    // 1: two-role exchange pass (sweepx.cuh): host builds a tile
+                                   //    table; maps.u1 = u^{n+1} box map over the level-1 output
 };
 
 // Defined in the generated instance translation units.
@@ -235,17 +235,16 @@ constexpr KernelEntry make_entry2() {
                      WAVE ? G::EBW : 0, WAVE ? G::GH : 0, WAVE ? G::OY : 0};
 }
 
-// ---- exchange-tiled kernel (sweept.cuh): T_k = 2, level-1 halo read back through L2
-template <int R, bool WAVE, int NCW, int VY, int D>
-cudaError_t launch_sweept(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
+// ---- two-role exchange pass (sweepx.cuh): T_k = 2 as L1 + L2 untiled sweeps through L2
+template <int R, bool WAVE, int NCW, int VY>
+cudaError_t launch_sweepx(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  (void)nslot;
-  return launch_pdl(sweept_kernel<R, WAVE, NCW, VY, D>, grid, 32 * (NCW + 3), smem, stream, maps.u, maps.u1, p);
+  return launch_pdl(sweepx_kernel<R, WAVE, NCW, VY>, grid, 32 * (NCW + 2), smem, stream, maps.u, maps.u1, p, nslot);
 }
 
-template <int R, bool WAVE, int NCW, int VY, int D>
-cudaError_t query_sweept(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
-  auto k = sweept_kernel<R, WAVE, NCW, VY, D>;
+template <int R, bool WAVE, int NCW, int VY>
+cudaError_t query_sweepx(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweepx_kernel<R, WAVE, NCW, VY>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (attr) {
@@ -256,13 +255,12 @@ cudaError_t query_sweept(size_t smem, cudaFuncAttributes* attr, int* bps, int nt
   return cudaSuccess;
 }
 
-template <int R, bool WAVE, int NCW, int VY, int D>
-constexpr KernelEntry make_entryT() {
-  using G = GeomT<R, NCW, VY, WAVE, D>;
-  KernelEntry e{3, WAVE ? 2 : 1, R, 2, VY, NCW, G::NTHREADS, 64, G::H, G::BW, G::BH,
-                R, (size_t)G::SLOT_BYTES, (size_t)(G::SMEM - G::NU * G::SLOT_BYTES),
-                &launch_sweept<R, WAVE, NCW, VY, D>, &query_sweept<R, WAVE, NCW, VY, D>, 0};
-  e.fixed_slots = G::NU;
+template <int R, bool WAVE, int NCW, int VY>
+constexpr KernelEntry make_entryX() {
+  using G = Geom1<R, 3, NCW, VY>;
+  KernelEntry e{3, WAVE ? 2 : 1, R, 2, VY, NCW, 32 * (NCW + 2), G::OX, G::OY, G::BW, G::BH,
+                R, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
+                &launch_sweepx<R, WAVE, NCW, VY>, &query_sweepx<R, WAVE, NCW, VY>, ST_T1_DEPTH};
   e.exch = 1;
   return e;
 }

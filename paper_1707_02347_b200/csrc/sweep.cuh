@@ -25,15 +25,6 @@ namespace st {
 
 constexpr int kMaxR = 8;
 
-// One tile of the exchange-tiled pass (sweept.cuh; built by abi.cu plan_tiles).
-struct TileDesc {
-  int x0, y0;             // level-1 region: columns [x0, x0+64), rows [y0, y0+H) (interior coords)
-  int l2_lo, l2_hi;       // rows whose level 2 (u^{n+2}) this tile produces
-  int st_lo, st_hi;       // rows whose level 1 (u^{n+1}) this tile stores
-  int zb, ze;             // level-2 output planes (array coordinates)
-  int dep[4];             // tiles whose stored level 1 feeds this tile's level-2 halo (-1: none)
-};
-
 struct SweepParams {
   int nx, ny;                 // interior extents (x, y)
   int X;                      // row pitch in floats (multiple of 32)
@@ -81,9 +72,9 @@ struct SweepParams {
   const unsigned long long* wait_hi;
   unsigned long long wait_lo_target, wait_hi_target;
   int iso;                    // W[0][k] == W[1][k] == W[2][k] bitwise for every k (isotropic dx)
-  // exchange-tiled pass (sweept.cuh): tile table, ticket counter, per-tile level-1 progress
-  // (values base + planes done, compared modulo 2^32), fault word of timed-out waits
-  const TileDesc* x_tiles;
+  // two-role exchange pass (sweepx.cuh): tile table (XTile[]), ticket counter, per-tile
+  // progress (base + stored-up-to plane, compared modulo 2^32), fault word of timed-out waits
+  const void* x_tiles;
   int x_ntiles;
   unsigned* x_ticket;
   unsigned x_ticket_base;

@@ -49,5 +49,5 @@ def test_alg_bytes_and_kernel_names():
     assert bench._alg_bytes_per_point_launch(c5, True, 2) == 24       # + one more output level
     assert bench._alg_bytes_per_point_launch(c2, False, 1) == 8
     assert bench._kernel_name(c5, 1).startswith("st::sweep1s_kernel<R=6")
-    assert bench._kernel_name(W.problem("C3"), 2).startswith("st::sweep2_kernel<R=4")
+    assert bench._kernel_name(W.problem("C3"), 2).startswith("st::sweepx_kernel<R=4")
     assert bench._kernel_name(W.problem("C4"), 1).startswith("st::sweep1s_kernel<R=8")
