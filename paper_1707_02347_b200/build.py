@@ -75,8 +75,9 @@ def _static_ring(ndim: int, wave: int, R: int) -> bool:
 
 def _exch(wave: int, R: int) -> bool:
     """T_k = 2 instances built as the two-role exchange pass (sweepx.cuh): wave r >= 3 (measured
-    faster than the overlapped-tile sweep2 at SO8 and SO12) and heat r <= 2."""
-    return (wave and R >= 3) or (not wave and R <= 2)
+    faster than the overlapped-tile sweep2 at SO8 and SO12; heat C2 measured 276 GPts/s vs 486 for
+    sweep2, so heat keeps sweep2 -- DESIGN.md §10)."""
+    return bool(wave) and R >= 3
 
 
 def instances():

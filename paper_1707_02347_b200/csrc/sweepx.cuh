@@ -40,12 +40,13 @@ struct XTile {                // one tile of an L1/L2 exchange pass (built by ab
   int partner;                // L1: the L2 tile of the same column and row index (throttle), or -1
 };
 
-// An L1 tile runs at most XLAG planes ahead of its partner L2 tile once that one has started,
-// so the u^{n+1}, u^n and a, c planes the L2 tiles re-read are still in L2 (the lag would
-// otherwise grow along the z stream and turn those reads into HBM reads).  XLAG > r + 1 keeps
-// the throttle deadlock-free (DESIGN.md §6 G3).
+// Optional throttle (off by default, ST_XLAG = 0): an L1 tile waits before loading plane p until
+// its partner L2 tile (if started) stored p - XLAG, bounding the L2 re-read window.  Measured
+// slower at every window tried (C3 T_k=2: 250 GPts/s without, 176 at 48, 117 at 32, 63 at 16)
+// because it couples every L1 tile to the publication latency of the L2 tiles.
+// A window must exceed the L2 tile's own lag, ~2r + its ring prefetch, or the pass stalls.
 #ifndef ST_XLAG
-#define ST_XLAG 16
+#define ST_XLAG 0
 #endif
 
 __device__ __forceinline__ unsigned ldx_relaxed_gpu(const unsigned* a) {
@@ -180,7 +181,7 @@ sweepx_kernel(const __grid_constant__ CUtensorMap tmapU, const __grid_constant__
       for (int a = 0; a < n_arr; ++a) {
         if (a >= nslot) mbar_wait(&empty[slot], ph ^ 1u);
         const int pl = p_first + a;                  // array plane of this box
-        if (!L2 && ok && td.partner >= 0 && pl - ST_XLAG >= thr_seen) {
+        if (ST_XLAG > 0 && !L2 && ok && td.partner >= 0 && pl - ST_XLAG >= thr_seen) {
           // throttle: wait until the partner L2 tile stored plane pl - XLAG, if it has started
           // (a partner that has not published in this launch reads below base: no wait)
           const long long t0 = clock64();
