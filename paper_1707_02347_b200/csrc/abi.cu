@@ -24,6 +24,7 @@
 
 #include "../../include/stencil.h"
 #include "registry.h"
+#include "resident.cuh"
 
 namespace {
 
@@ -673,6 +674,29 @@ static void plan_xtiles(const stencil_plan* p, const st::KernelEntry* k, int out
   }
 }
 
+// ------------------------------------------------------------------ resident 2-D run (G4)
+extern "C++" {
+typedef void (*res_kernel_t)(const st::SweepParams, float*, float*, int);
+template <int R>
+static res_kernel_t res_pick(bool wave) {
+  return wave ? &st::resident2d_kernel<R, true> : &st::resident2d_kernel<R, false>;
+}
+static res_kernel_t res_kernel(int R, bool wave) {
+  switch (R) {
+    case 1: return res_pick<1>(wave); case 2: return res_pick<2>(wave);
+    case 3: return res_pick<3>(wave); case 4: return res_pick<4>(wave);
+    case 5: return res_pick<5>(wave); case 6: return res_pick<6>(wave);
+    case 7: return res_pick<7>(wave); default: return res_pick<8>(wave);
+  }
+}
+// whole run of a 2-D plan in one CTA when both time levels (+ medium) fit in shared memory
+static bool res_fits(const stencil_plan* p) {
+  if (p->cfg.ndim != 2 || p->cfg.nranks != 1) return false;
+  if (getenv("ST_NO_RESIDENT")) return false;   // test/measurement override: per-step sweeps
+  return st::res_smem_bytes(p->cfg.radius, p->cfg.time_order == 2, (int)p->nx, (int)p->ny) <= 227 * 1024;
+}
+}  // extern "C++"
+
 static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,
                           const float* damp, int32_t nt, int64_t step0, int32_t nsrc,
                           const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
@@ -762,6 +786,7 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
 
   int j = 0;
   int launches = 0, tiled_launches = 0;
+  const bool resident = save_every <= 0 && !fused && res_fits(p);
   cudaEvent_t t_ev1 = nullptr;
   if (p->timing) {
     if ((int)p->ev_pool.size() < 2 * (p->ev_used + 1)) {
@@ -773,6 +798,21 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
     }
     CK(cudaEventRecord(p->ev_pool[2 * p->ev_used], p->stream), "timing event");
     t_ev1 = p->ev_pool[2 * p->ev_used + 1];
+  }
+  if (resident) {
+    // G4: all nt steps in shared memory, one launch; the kernel writes (u^{n+nt-1}, u^{n+nt})
+    // straight into (u_prev, u_cur)
+    sp.wl_step = step0;
+    sp.tr_step = 0;
+    sp.out_lo = (int)p->G; sp.out_hi = (int)(p->G + p->nzl);
+    const size_t smem = st::res_smem_bytes(c.radius, wave, (int)p->nx, (int)p->ny);
+    res_kernel_t kf = res_kernel(c.radius, wave);
+    CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "resident smem");
+    CK(st::launch_pdl(kf, dim3(1), st::RES_THREADS, smem, p->stream, sp, u_prev, u_cur, (int)nt),
+       "resident kernel launch");
+    ++launches;
+    tiled_launches += 1;
+    j = nt;
   }
   while (j < nt) {
     // a time-tiled pass never crosses a snapshot step (passes end on multiples of save_every)

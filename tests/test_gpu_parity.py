@@ -215,3 +215,29 @@ def test_snapshots_match_oracle(tk, every):
     _, want_c, _ = oracle_run(p)
     assert np.array_equal(st.interior(C).cpu().numpy(), want_c)
     st.close()
+
+
+# ----------------------------------------------------------------------------- G4 resident 2-D
+@pytest.mark.parametrize("resident", [True, False])
+@pytest.mark.parametrize("order,n", [(2, (77, 53, 1)), (8, (64, 40, 1)), (16, (41, 47, 1))])
+def test_2d_wave_resident_vs_per_step(monkeypatch, resident, order, n):
+    """2-D wave through the whole-run shared-memory kernel (G4) and, with ST_NO_RESIDENT, through
+    the per-step sweeps: ragged odd widths, sources on the first/last column (pair lo/hi element),
+    duplicate sources, receivers on corners -- bit-exact vs the oracle either way."""
+    if not resident:
+        monkeypatch.setenv("ST_NO_RESIDENT", "1")
+    nx, ny, _ = n
+    p = W.problem("C1", n=n, nt=13)
+    d = dict(p.__dict__, time_order=2, space_order=order, dt=8e-4, dx=(10.0, 12.0, 10.0), init="zero",
+             layers=(1500.0, 2500.0, 3500.0, 4500.0), f_peak=15.0, sponge=6,
+             src=((nx // 2, ny // 2, 0), (0, 3, 0), (nx - 1, ny - 2, 0), (nx // 2, ny // 2, 0)),
+             rec=((0, 0, 0), (nx - 1, ny - 1, 0), (nx // 2, ny // 2, 0), (1, ny - 1, 0)))
+    _check(W.Problem(**d))
+
+
+@pytest.mark.parametrize("resident", [True, False])
+def test_2d_heat_resident_eigenmode(monkeypatch, resident):
+    if not resident:
+        monkeypatch.setenv("ST_NO_RESIDENT", "1")
+    p = W.problem("C1", n=(99, 128, 1), nt=37)
+    _check(W.Problem(**dict(p.__dict__, init="eigenmode")))
