@@ -139,6 +139,12 @@ def run_gpu(args):
     from paper_1707_02347_b200.planner import plan
     pl = plan(p.time_order, p.radius, p.n, nranks=world, ndim=p.ndim)
     tk = pl.t_kernel if args.tk == "auto" else int(args.tk)
+    from paper_1707_02347_b200.stencil import supported
+    if not supported(p.ndim, p.time_order, p.radius, tk):
+        ok = [t for t in (1, 2, 4, 8) if supported(p.ndim, p.time_order, p.radius, t)]
+        raise SystemExit(f"bench.py: t_kernel={tk} is not built for {args.config} "
+                         f"(ndim={p.ndim}, time_order={p.time_order}, radius={p.radius}); "
+                         f"compiled depths: {ok} (DESIGN.md §6: wave time tiles are T_k <= 2)")
     if world > 1:
         tc = pl.t_comm if args.tc is None else max(tk, args.tc)
         tc = tc if tc % tk == 0 else tk * ((tc + tk - 1) // tk)
@@ -150,7 +156,7 @@ def run_gpu(args):
     st = runner.stencil
     # ---- host inputs (pinned) for this rank's slab, then resident device copies ----------------
     host = runner.host_inputs(nt, pin=True)
-    dev_in = runner.to_device(host)
+    dev_in = runner.to_device(host, nt)
     fused = runner.enable_fused(dev_in) if args.fused_halo else False
 
     def step_resident():
@@ -312,36 +318,87 @@ def _oracle_inputs(cfg: str):
     return p, P0, C0, a, c, wv
 
 
-def _oracle_steps(p, P0, C0, a, c, wv, nt):
-    """O1 as it stands: nt time steps of the full grid from the initial state."""
+def _cpu_info():
+    """CPU model, logical cores, and the oracle's OpenMP thread count (PAPER states its machine,
+    P:1581-1588; so does this baseline)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
     import oracle
-    P, C = P0.copy(), C0.copy()
-    oracle.run_untiled(p.ndim, p.n, p.space_order, oracle.fd_weights(p.space_order), p.dx,
-                       p.time_order, p.dt, P, C, a, c, nt=nt, src=list(p.src), wavelet=wv,
-                       rec=list(p.rec))
+    return {"cpu_model": model, "nproc": os.cpu_count(), "omp_threads": oracle.num_threads()}
+
+
+_ONE_THREAD = r"""
+import sys, time
+sys.path.insert(0, sys.argv[1])
+import numpy as np, oracle, workloads as W
+p = W.problem("C3")
+r = p.radius
+P = oracle.embed(np.zeros((p.n[2], p.n[1], p.n[0]), np.float32), 3, r)
+C = P.copy()
+vel = oracle.embed(W.velocity(p), 3, r); vel[vel == 0] = 1.0
+a, c = oracle.medium(vel, oracle.embed(W.damp(p), 3, r), p.dt)
+wv = W.wavelet(p)
+t0 = time.perf_counter()
+oracle.run_untiled(3, p.n, p.space_order, oracle.fd_weights(p.space_order), p.dx, 2, p.dt, P, C, a, c,
+                   nt=2, src=list(p.src), wavelet=wv)
+dt = time.perf_counter() - t0
+print(p.points * 2 / dt / 1e9, oracle.num_threads())
+"""
+
+
+def one_thread_rate():
+    """The oracle O1 on ONE host thread: C3 (SO8 512^3), 2 time steps."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        r = subprocess.run([sys.executable, "-c", _ONE_THREAD, ROOT], capture_output=True, text=True,
+                           env=env, timeout=600)
+        v, th = r.stdout.strip().split()[-2:]
+        return {"value": round(float(v), 4), "unit": "GPts/s", "threads": int(th),
+                "sample": "C3 full grid 512^3 SO8, 2 of 500 time steps, OMP_NUM_THREADS=1"}
+    except Exception as e:   # reported, not fatal: the baseline is context
+        return {"value": None, "error": str(e)[:200]}
 
 
 def cpu_baseline(cfg: str, seconds: float = 15.0):
     """The oracle O1 as it stands, on this host's cores, on a bounded sample of the workload:
-    the full grid for as many time steps as fit in ~`seconds` (>= 1); input generation untimed."""
+    the full grid for as many time steps as fit in ~`seconds` (>= 1); input generation and the
+    state copies untimed."""
     import oracle
     ins = _oracle_inputs(cfg)
     p = ins[0]
-    t0 = time.perf_counter()
-    _oracle_steps(*ins, nt=1)                      # calibration step
-    one = time.perf_counter() - t0
+    one = _oracle_timed(*ins, nt=1)                # calibration step
     steps = max(1, min(p.nt, int(seconds / max(one, 1e-3))))
+    dt = _oracle_timed(*ins, nt=steps)
+    out = {"value": round(p.points * steps / dt / 1e9, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
+           "kind": "oracle",
+           "sample": f"{cfg} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {steps} of {p.nt} time steps from the "
+                     f"seeded initial state (O1 loop nest only; input generation and state copies untimed)"}
+    out.update(_cpu_info())
+    out["one_thread"] = one_thread_rate()
+    return out
+
+
+def _oracle_timed(p, P0, C0, a, c, wv, nt):
+    """Seconds of O1 for nt steps from the initial state; the state copies are not timed."""
+    import oracle
+    P, C = P0.copy(), C0.copy()
     t0 = time.perf_counter()
-    _oracle_steps(*ins, nt=steps)
-    dt = time.perf_counter() - t0
-    return {"value": round(p.points * steps / dt / 1e9, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
-            "kind": "oracle",
-            "sample": f"{cfg} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {steps} of {p.nt} time steps from the "
-                      f"seeded initial state (O1 loop nest only; input generation untimed)"}
+    oracle.run_untiled(p.ndim, p.n, p.space_order, oracle.fd_weights(p.space_order), p.dx,
+                       p.time_order, p.dt, P, C, a, c, nt=nt, src=list(p.src), wavelet=wv,
+                       rec=list(p.rec))
+    return time.perf_counter() - t0
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle arm, timed per bench step on a bounded sample."""
+    """--impl reference: the CPU oracle arm, timed per bench step on a bounded sample (the
+    config's full grid for --ref-steps time steps; state copies outside the timed region)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
@@ -349,18 +406,15 @@ def run_reference(args):
     ins = _oracle_inputs(args.config)
     p = ins[0]
     sample_steps = args.ref_steps
-
-    def one():
-        _oracle_steps(*ins, nt=sample_steps)
     for _ in range(args.warmup):
-        one()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
-    dt = time.perf_counter() - t0
+        _oracle_timed(*ins, nt=sample_steps)
+    dt = sum(_oracle_timed(*ins, nt=sample_steps) for _ in range(args.steps))
     value = p.points * sample_steps * args.steps / dt / 1e9
     sample = (f"{args.config} full grid {p.n[0]}x{p.n[1]}x{p.n[2]}, {sample_steps} of {p.nt} time steps per "
-              f"bench step (bounded sample of the workload)")
+              f"bench step (bounded sample of the workload; state copies untimed)")
+    cb = {"value": round(value, 4), "unit": "GPts/s", "cores": oracle.num_threads(), "kind": "oracle",
+          "sample": sample}
+    cb.update(_cpu_info())
     return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GPts/s",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
@@ -368,8 +422,7 @@ def run_reference(args):
             "data": "synthetic (workloads/, seeded)",
             "config": {"workload": f"{args.config}: {_describe(p)}", "grid": list(p.n),
                        "nt_per_step": sample_steps, "space_order": p.space_order},
-            "cpu_baseline": {"value": round(value, 4), "unit": "GPts/s", "cores": oracle.num_threads(),
-                             "kind": "oracle", "sample": sample},
+            "cpu_baseline": cb,
             "e2e": {"value": round(value, 4), "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -385,7 +438,7 @@ def main():
     ap.add_argument("--so", type=int, default=None, help="override the space order (study runs only)")
     ap.add_argument("--grid", default=None, help="override the interior grid, e.g. 512x512x512 (study runs only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-steps", type=int, default=2, help="time steps per reference bench step")
+    ap.add_argument("--ref-steps", type=int, default=5, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fused-halo", action="store_true",
                     help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")

@@ -80,7 +80,7 @@ struct stencil_plan {
   cudaEvent_t staging_ev = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   bool broken = false;
-  std::string err;
+  mutable std::string err;             // also set by the const entry points (stencil_ipc_export)
   // timing (stencil_set_timing / stencil_timing)
   // one (start, end) event pair per timed run since the last stencil_timing query; the pool is
   // reused, so a run records events without any host synchronisation
@@ -92,7 +92,7 @@ struct stencil_plan {
 
 namespace {
 
-st_status fail(stencil_plan* p, st_status s, const char* fmt, ...) {
+st_status fail(const stencil_plan* p, st_status s, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -313,20 +313,20 @@ st_status stencil_set_peer(stencil_plan* p, int32_t side, const float* my_a, con
 }
 
 st_status stencil_ipc_export(const stencil_plan* p, const void* dev_ptr, void* blob) {
-  if (!p || !dev_ptr || !blob) return fail(nullptr, ST_EINVAL, "null argument");
-  if (cudaSetDevice(p->device) != cudaSuccess) return fail(nullptr, ST_ECUDA, "cudaSetDevice failed");
+  if (!p || !dev_ptr || !blob) return fail(p, ST_EINVAL, "null argument");
+  if (cudaSetDevice(p->device) != cudaSuccess) return fail(p, ST_ECUDA, "cudaSetDevice failed");
   // base of the allocation holding dev_ptr (torch's caching allocator sub-allocates segments)
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-    return fail(nullptr, ST_ECUDA, "cuMemGetAddressRange lookup failed");
+    return fail(p, ST_ECUDA, "cuMemGetAddressRange lookup failed");
   CUdeviceptr base = 0;
   size_t size = 0;
   if (reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn)(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
-    return fail(nullptr, ST_ECUDA, "cuMemGetAddressRange failed for %p", dev_ptr);
+    return fail(p, ST_ECUDA, "cuMemGetAddressRange failed for %p", dev_ptr);
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
-  if (e != cudaSuccess) return fail(nullptr, ST_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(p, ST_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
   const long long off = (long long)((CUdeviceptr)dev_ptr - base);
   memcpy(blob, &h, sizeof h);
   memcpy(static_cast<char*>(blob) + 64, &off, sizeof off);

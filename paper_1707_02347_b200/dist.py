@@ -161,12 +161,16 @@ class SlabRunner:
             out["wavelet"] = w.pin_memory() if pin else w
         return out
 
-    def to_device(self, host: Dict[str, torch.Tensor]) -> Dict[str, torch.Tensor]:
+    def to_device(self, host: Dict[str, torch.Tensor], nt: int = None) -> Dict[str, torch.Tensor]:
+        """Device copies of host_inputs(nt); the receiver trace is sized for nt steps (default: the
+        wavelet's row count, else the problem's nt), so run(dev, nt) never writes past it."""
         dev = {k: v.to(f"cuda:{self.device}", non_blocking=True) for k, v in host.items()}
         dev["_init_cur"] = dev["u_cur"].clone()
         dev["_init_prev"] = dev["u_prev"].clone()
+        if nt is None:
+            nt = host["wavelet"].shape[0] if "wavelet" in host else self.p.nt
         if self.p.rec:
-            dev["trace"] = torch.zeros((max(1, self.p.nt), len(self.p.rec)), dtype=torch.float32,
+            dev["trace"] = torch.zeros((max(1, nt), len(self.p.rec)), dtype=torch.float32,
                                        device=f"cuda:{self.device}")
         return dev
 

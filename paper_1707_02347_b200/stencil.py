@@ -117,6 +117,13 @@ class Stencil:
         nrec, rec_a = _points(rec)
         if nrec and trace is None:
             trace = torch.zeros((nt, nrec), dtype=torch.float32, device=u_cur.device)
+        # the C ABI cannot check buffer lengths: a short trace or wavelet would be overrun
+        if nrec and (trace.dim() != 2 or trace.shape[0] < nt or trace.shape[1] != nrec):
+            raise ValueError(f"trace must be [>= nt={nt}, nrec={nrec}] (got {tuple(trace.shape)})")
+        if nsrc and (wavelet is None or wavelet.dim() != 2 or wavelet.shape[0] < step0 + nt
+                     or wavelet.shape[1] != nsrc):
+            got = None if wavelet is None else tuple(wavelet.shape)
+            raise ValueError(f"wavelet must be [>= step0+nt={step0 + nt}, nsrc={nsrc}] (got {got})")
         lib = _lib.load()
         args = (self._h, _ptr(u_prev), _ptr(u_cur), _ptr(vel), _ptr(damp), int(nt), int(step0), nsrc,
                 None if src_a is None else src_a.ctypes.data_as(ctypes.c_void_p), _ptr(wavelet), nrec,

@@ -189,13 +189,15 @@ def test_paper_replica_full_grid(name, nt):
 
 
 # ----------------------------------------------------------------------------- snapshots (save mode)
-@pytest.mark.parametrize("tk,every", [(1, 3), (2, 3), (2, 4), (1, 1)])
-def test_snapshots_match_oracle(tk, every):
+@pytest.mark.parametrize("tk,every,order", [(1, 3, 8), (2, 3, 8), (2, 4, 8), (1, 1, 8),
+                                            (1, 3, 12), (2, 2, 12), (1, 2, 16), (2, 4, 16)])
+def test_snapshots_match_oracle(tk, every, order):
     """stencil_run_save: snapshot j holds u^{j*every} bit-exactly (oracle run of j*every steps);
-    the run's final state is unchanged by saving (SURVEY §8(f) NEXT-2 ii)."""
+    the run's final state is unchanged by saving (SURVEY §8(f) NEXT-2 ii).  SO12/SO16 cover the
+    snapshot-store instances of the static-ring untiled kernel and of the exchange pass."""
     import torch
     from paper_1707_02347_b200 import Stencil
-    p = _wave("C3", (45, 38, 30), 10, 5, src=[(22, 19, 15)], rec=[(20, 20, 20)])
+    p = _wave("C3", (45, 38, 30), 10, 5, order=order, src=[(22, 19, 15)], rec=[(20, 20, 20)])
     st = Stencil(p.ndim, p.n, p.space_order, p.time_order, p.dt, p.dx, t_kernel=tk)
     up, uc = W.initial_fields(p)
     P = st.embed(torch.from_numpy(up).cuda())
