@@ -162,11 +162,9 @@ def _digest(paths, extra=()):
 
 def _compile(src: str, outdir: str = BUILD, defines=()):
     obj = os.path.join(outdir, os.path.basename(src) + ".o")
-    deps = [src, os.path.join(CSRC, "sweep.cuh"), os.path.join(CSRC, "sweep1.cuh"),
-            os.path.join(CSRC, "sweep2.cuh"), os.path.join(CSRC, "sweep1s.cuh"),
-            os.path.join(CSRC, "sweepx.cuh"),
-            os.path.join(CSRC, "registry.h"),
-            os.path.join(HERE, "..", "include", "stencil.h")]
+    # every header of csrc/ and the ABI header: any edit rebuilds every object that may include it
+    deps = [src] + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) \
+        + [os.path.join(HERE, "..", "include", "stencil.h")]
     stamp = obj + ".stamp"
     d = _digest(deps, defines)
     if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == d:

@@ -220,19 +220,25 @@ def test_snapshots_match_oracle(tk, every, order):
 
 
 # ----------------------------------------------------------------------------- G4 resident 2-D
-@pytest.mark.parametrize("resident", [True, False])
-@pytest.mark.parametrize("order,n", [(2, (77, 53, 1)), (8, (64, 40, 1)), (16, (41, 47, 1))])
+@pytest.mark.parametrize("resident", ["spb", "1", "2", "off"])
+@pytest.mark.parametrize("order,n", [(2, (77, 53, 1)), (8, (64, 40, 1)), (16, (41, 47, 1)),
+                                     (4, (128, 128, 1))])
 def test_2d_wave_resident_vs_per_step(monkeypatch, resident, order, n):
-    """2-D wave through the whole-run shared-memory kernel (G4) and, with ST_NO_RESIDENT, through
-    the per-step sweeps: ragged odd widths, sources on the first/last column (pair lo/hi element),
-    duplicate sources, receivers on corners -- bit-exact vs the oracle either way."""
-    if not resident:
+    """2-D wave through the whole-run cluster-resident kernel (G4: rows split over up to 8 CTAs,
+    DSMEM halo push every spb steps, redundant halo rows in between; ST_RES_SPB caps spb) and,
+    with ST_NO_RESIDENT, through the per-step sweeps: ragged odd widths, sources on the first/last
+    column (pair lo/hi element) and on CTA-boundary rows, duplicate sources, receivers on corners
+    -- bit-exact vs the oracle either way."""
+    if resident == "off":
         monkeypatch.setenv("ST_NO_RESIDENT", "1")
+    elif resident != "spb":
+        monkeypatch.setenv("ST_RES_SPB", resident)
     nx, ny, _ = n
     p = W.problem("C1", n=n, nt=13)
     d = dict(p.__dict__, time_order=2, space_order=order, dt=8e-4, dx=(10.0, 12.0, 10.0), init="zero",
              layers=(1500.0, 2500.0, 3500.0, 4500.0), f_peak=15.0, sponge=6,
-             src=((nx // 2, ny // 2, 0), (0, 3, 0), (nx - 1, ny - 2, 0), (nx // 2, ny // 2, 0)),
+             src=((nx // 2, ny // 2, 0), (0, 3, 0), (nx - 1, ny - 2, 0), (nx // 2, ny // 2, 0),
+                  (5, 7, 0), (6, 8, 0), (nx - 3, 16, 0)),
              rec=((0, 0, 0), (nx - 1, ny - 1, 0), (nx // 2, ny // 2, 0), (1, ny - 1, 0)))
     _check(W.Problem(**d))
 
