@@ -22,8 +22,14 @@
 
 namespace st {
 
-constexpr int RES_THREADS = 512;
-constexpr int RES_CLUSTER = 8;     // CTAs per cluster (portable maximum)
+#ifndef ST_RES_THREADS
+#define ST_RES_THREADS 512
+#endif
+constexpr int RES_THREADS = ST_RES_THREADS;
+#ifndef ST_RES_CLUSTER
+#define ST_RES_CLUSTER 16
+#endif
+constexpr int RES_CLUSTER = ST_RES_CLUSTER;   // CTAs per cluster (16: B200's non-portable maximum)
 #ifndef ST_RES_STRIP
 #define ST_RES_STRIP 2
 #endif
@@ -45,9 +51,9 @@ __host__ __device__ inline size_t res_smem_bytes(int R, bool wave, int nx, int n
   const size_t flags = ((size_t)((nx + 1) >> 1) * rows + 31) / 32 * 4;   // source-pair bitmap
   return 2 * field + medium + flags;
 }
-// cluster size: as many CTAs (<= RES_CLUSTER) as keep >= r own rows each
-__host__ __device__ inline int res_cluster(int R, int ny) {
-  int cs = RES_CLUSTER;
+// cluster size: as many CTAs (<= cap) as keep >= r own rows each
+__host__ __device__ inline int res_cluster(int R, int ny, int cap = RES_CLUSTER) {
+  int cs = cap;
   while (cs > 1 && (res_own(ny, cs) < R || (cs - 1) * res_own(ny, cs) >= ny)) --cs;
   return cs;
 }
@@ -191,6 +197,8 @@ resident2d_kernel(const __grid_constant__ SweepParams p, float* __restrict__ u_p
   cluster.sync();
 
   constexpr int S = RES_STRIP;
+  const bool fixed_map = RES_THREADS % pr == 0;
+  const int xp0 = tid % pr, sj0 = tid / pr, sstep = RES_THREADS / pr;
   float* cur = B1;
   float* oth = B0;
   int off = 0;                                   // oth - B0 (same offset in every CTA)
@@ -201,13 +209,22 @@ resident2d_kernel(const __grid_constant__ SweepParams p, float* __restrict__ u_p
       // local rows of this sub-step: the halo shrinks by r per step, never outside the grid
       const int ext = R * (steps - 1 - j);
       const int lr0 = max(-ext, -r0), lr1 = min(nrow + ext, ny - r0);
-      const int items = pr * ((lr1 - lr0 + S - 1) / S);
-      for (int t = tid; t < items; t += RES_THREADS) {
-        const int sj = t / pr, xp = t - sj * pr;
-        const int x = 2 * xp;
-        const int lr = lr0 + sj * S;
-        res_strip<R, WAVE, S>(cur, oth, Am, Cm, pitch, nx2, x, lr + H, r0 + lr, r0 + lr1, HL,
-                              p, sflag, pr, wl, x + 1 >= nx);
+      // thread -> (column pair xp0, first strip sj0), then strips sj0 + k*sstep (no division in
+      // the loop when the threads cover whole rows of pairs)
+      const int nstr = (lr1 - lr0 + S - 1) / S;
+      if (fixed_map) {
+        for (int sj = sj0; sj < nstr; sj += sstep) {
+          const int lr = lr0 + sj * S;
+          res_strip<R, WAVE, S>(cur, oth, Am, Cm, pitch, nx2, 2 * xp0, lr + H, r0 + lr, r0 + lr1, HL,
+                                p, sflag, pr, wl, 2 * xp0 + 1 >= nx);
+        }
+      } else {
+        for (int t = tid; t < pr * nstr; t += RES_THREADS) {
+          const int sj = t / pr, xp = t - sj * pr;
+          const int lr = lr0 + sj * S;
+          res_strip<R, WAVE, S>(cur, oth, Am, Cm, pitch, nx2, 2 * xp, lr + H, r0 + lr, r0 + lr1, HL,
+                                p, sflag, pr, wl, 2 * xp + 1 >= nx);
+        }
       }
       __syncthreads();
       for (int k = rb + tid; k < re; k += RES_THREADS) {
