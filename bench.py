@@ -152,7 +152,7 @@ def run_gpu(args):
         tc = tk
     nt = p.nt if args.nt is None else args.nt
     runner = SlabRunner(p, rank=rank, world=world, t_kernel=tk, t_comm=tc, device=local,
-                        fused=args.fused_halo)
+                        fused=args.fused_halo, lib_exchange=args.lib_exchange)
     st = runner.stencil
     # ---- host inputs (pinned) for this rank's slab, then resident device copies ----------------
     host = runner.host_inputs(nt, pin=True)
@@ -244,6 +244,8 @@ def run_gpu(args):
                 "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
                 "halo": (None if world == 1 else
                          "fused push: sweep stores band planes into peer ghost zones (P2P)" if fused
+                         else "library-owned NCCL exchange (bands overlapped with the interior)"
+                         if runner.lib_exchange
                          else "NCCL send/recv of contiguous ghost planes every T_c steps"),
                 "l2": "inputs larger than L2 (fields %.0f MiB each, L2 126 MB); no flush" % (
                     runner.field_bytes / 2**20),
@@ -279,7 +281,10 @@ def _describe(p: W.Problem) -> str:
 
 
 def _kernel_name(p: W.Problem, tk: int) -> str:
-    """Name of the compiled sweep instance a pass of this problem launches (build.instances())."""
+    """Name of the compiled sweep instance a pass of this problem launches (build.instances());
+    2-D grids that fit a thread-block cluster's shared memory run the resident kernel (G4)."""
+    if p.ndim == 2 and not os.environ.get("ST_NO_RESIDENT"):
+        return f"st::resident2d_kernel<R={p.radius}, wave={int(p.time_order == 2)}> (whole run)"
     from paper_1707_02347_b200.build import instances
     names = {0: "st::sweep_kernel", 1: "st::sweep1_kernel", 2: "st::sweep2_kernel", 3: "st::sweep1s_kernel",
              4: "st::sweepx_kernel"}
@@ -442,6 +447,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fused-halo", action="store_true",
                     help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")
+    ap.add_argument("--lib-exchange", action="store_true",
+                    help="N > 1: the library owns the NCCL halo exchange and the time loop "
+                         "(st_config.nccl_id; boundary bands overlapped with the interior at T_c = 1)")
     args = ap.parse_args()
     _OVERRIDE.update(so=args.so, n=args.grid)
     if args.warmup < 3:

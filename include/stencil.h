@@ -56,6 +56,7 @@ typedef enum {
   ST_EINVAL = 1,          /* bad argument (null pointer, radius, sizes, coordinates, nt) */
   ST_ENOMEM = 2,          /* device or host allocation failed */
   ST_ECUDA = 3,           /* a CUDA runtime/driver call failed (message has the CUDA error) */
+  ST_ENCCL = 4,           /* NCCL could not be loaded or a NCCL call failed (message has details) */
   ST_EUNSUPPORTED = 5,    /* (radius, t_kernel, ndim, time_order) not compiled into this build */
   ST_ESTATE = 6           /* plan is in an error state after an asynchronous failure */
 } st_status;
@@ -81,7 +82,17 @@ typedef struct {
   int32_t device;         /* CUDA device ordinal */
   void *stream;           /* cudaStream_t all work is enqueued on (NULL = legacy default) */
   uint32_t flags;         /* ST_FTZ (must be set) | ST_NO_SWAP (optional) */
+  const void *nccl_id;    /* host ncclUniqueId (ST_NCCL_ID_BYTES bytes, e.g. from
+                             stencil_nccl_unique_id on rank 0, broadcast by the caller) or NULL.
+                             With nranks > 1 and nccl_id != NULL the LIBRARY owns the halo
+                             exchange: stencil_create joins a NCCL communicator (collective: every
+                             rank creates its plan concurrently), stencil_run takes any nt, loops
+                             over T_c-step periods internally and sums the receiver trace over the
+                             ranks (every rank gets the full trace).  NULL: the caller exchanges
+                             ghost planes between runs of at most t_comm steps. */
 } st_config;
+
+#define ST_NCCL_ID_BYTES 128
 
 /* Validate cfg, pick the compiled kernel instance, allocate scratch.  *out = NULL on error.
  * Errors: ST_EINVAL (null cfg/out/coeffs, ndim, radius outside 1..8, t_kernel < 1,
@@ -108,8 +119,14 @@ st_status stencil_layout(const stencil_plan *p, int64_t padded[3], int64_t inter
  *   rec_xyz       : host int32 [nrec][3], GLOBAL interior coordinates
  *   rec_trace     : device fp32 [nt][nrec]; row n = u^{n+1} at each receiver this rank owns;
  *                   entries of receivers owned by other ranks are not written.
- * nranks > 1: the caller must have exchanged ghost planes before the call (depth
+ * nranks > 1 without nccl_id: the caller must have exchanged ghost planes before the call (depth
  *   radius*nt of u_cur and radius*(nt-1) of u_prev), and nt <= t_comm.
+ * nranks > 1 with nccl_id (library-owned exchange): any nt; every rank calls with the same nt,
+ *   step0 and lists.  Each T_c period starts with a NCCL send/recv of the ghost planes on the
+ *   plan's comm stream; with t_comm == t_kernel == 1 the exchange of the next level is overlapped
+ *   with the interior: the r boundary planes of each side are swept first, their NCCL transfer
+ *   runs on the comm stream while the interior planes are swept, and the next step waits for it.
+ *   rec_trace is zeroed and then summed over the ranks (ncclAllReduce), so every rank holds it.
  * Asynchronous on cfg.stream; arguments must stay valid until it completes.
  * Source/receiver tables are rebuilt and uploaded only when src_xyz / rec_xyz differ from the
  * previous run's lists.
@@ -203,6 +220,11 @@ int32_t stencil_supported(int32_t ndim, int32_t time_order, int32_t radius, int3
 
 /* Pure host query: library ABI version (major*100 + minor). */
 int32_t stencil_abi_version(void);
+
+/* Fill out[ST_NCCL_ID_BYTES] with a fresh ncclUniqueId (ncclGetUniqueId of the NCCL the process
+ * has loaded, dlopen'ed as libnccl.so.2 or $ST_NCCL_LIB).  Host only; ST_ENCCL if NCCL is not
+ * available.  Rank 0 calls it and passes the bytes to every rank's st_config.nccl_id. */
+st_status stencil_nccl_unique_id(void *out);
 
 #ifdef __cplusplus
 }

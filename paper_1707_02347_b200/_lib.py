@@ -11,18 +11,19 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ST_LIB") or os.path.join(HERE, "libstencil.so")   # ST_LIB: experiment builds
 
-ST_OK, ST_EINVAL, ST_ENOMEM, ST_ECUDA, ST_EUNSUPPORTED, ST_ESTATE = 0, 1, 2, 3, 5, 6
+ST_OK, ST_EINVAL, ST_ENOMEM, ST_ECUDA, ST_ENCCL, ST_EUNSUPPORTED, ST_ESTATE = 0, 1, 2, 3, 4, 5, 6
 ST_FTZ = 1
 ST_NO_SWAP = 2
-STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 5: "ST_EUNSUPPORTED",
-                6: "ST_ESTATE"}
+STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 4: "ST_ENCCL",
+                5: "ST_EUNSUPPORTED", 6: "ST_ESTATE"}
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_run_save", "stencil_sync",
            "stencil_destroy", "stencil_last_error", "stencil_supported", "stencil_abi_version",
            "stencil_set_timing", "stencil_timing", "stencil_swapped", "stencil_peer_counters",
-           "stencil_set_peer", "stencil_ipc_export", "stencil_ipc_open")
+           "stencil_set_peer", "stencil_ipc_export", "stencil_ipc_open", "stencil_nccl_unique_id")
 ST_IPC_BYTES = 72
+ST_NCCL_ID_BYTES = 128
 
 
 class StConfig(ctypes.Structure):
@@ -41,6 +42,7 @@ class StConfig(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("flags", ctypes.c_uint32),
+        ("nccl_id", ctypes.c_void_p),
     ]
 
 
@@ -98,6 +100,8 @@ def load():
     lib.stencil_swapped.restype = ctypes.c_int32
     lib.stencil_abi_version.argtypes = []
     lib.stencil_abi_version.restype = ctypes.c_int32
+    lib.stencil_nccl_unique_id.argtypes = [P]
+    lib.stencil_nccl_unique_id.restype = ctypes.c_int
     _lib = lib
     return lib
 

@@ -105,16 +105,24 @@ class SlabRunner:
     planes every T_c steps.  world == 1 degenerates to a single stencil_run per simulation."""
 
     def __init__(self, problem, rank: int = 0, world: int = 1, t_kernel: int = 1, t_comm: int = 1,
-                 device: int = 0, fused: bool = False):
-        from .stencil import Stencil
+                 device: int = 0, fused: bool = False, lib_exchange: bool = False):
+        from .stencil import Stencil, nccl_unique_id
         self.p = problem
         self.rank, self.world = rank, world
         self.tk = t_kernel
         self.tc = t_comm if world > 1 else max(1, t_kernel)
         self.device = device
+        # lib_exchange: the library owns the NCCL communicator and the whole time loop
+        # (st_config.nccl_id); rank 0 makes the id, the process group broadcasts it
+        nccl_id = None
+        self.lib_exchange = lib_exchange and world > 1
+        if self.lib_exchange:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
         self.stencil = Stencil(problem.ndim, problem.n, problem.space_order, problem.time_order,
                                problem.dt, problem.dx, t_kernel=t_kernel, t_comm=self.tc, rank=rank,
-                               nranks=world, device=device, no_swap=True)
+                               nranks=world, device=device, no_swap=True, nccl_id=nccl_id)
         st = self.stencil
         self.G = st.G
         self.nzl = st.nz_local
@@ -240,6 +248,14 @@ class SlabRunner:
         if trace is not None:
             trace = trace[:nt]
             trace.zero_()
+        if self.lib_exchange:
+            # one C-ABI call: the library exchanges every T_c steps (overlapped at T_c = 1) and
+            # sums the trace over the ranks itself
+            st.run(dev["u_prev"], dev["u_cur"], nt, vel=dev.get("vel"), damp=dev.get("damp"),
+                   step0=0, src=list(p.src), wavelet=dev.get("wavelet"), rec=list(p.rec), trace=trace)
+            if st.swapped():
+                dev["u_prev"], dev["u_cur"] = dev["u_cur"], dev["u_prev"]
+            return trace
         done = 0
         while done < nt:
             n = min(self.tc, nt - done) if self.world > 1 else nt - done

@@ -36,7 +36,8 @@ class Stencil:
     def __init__(self, ndim: int, n: Sequence[int], space_order: int, time_order: int, dt: float,
                  dx: Sequence[float], t_kernel: int = 1, t_comm: int = 1, rank: int = 0,
                  nranks: int = 1, device: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None,
-                 coeffs: Optional[Sequence[float]] = None, no_swap: bool = False):
+                 coeffs: Optional[Sequence[float]] = None, no_swap: bool = False,
+                 nccl_id: Optional[bytes] = None):
         lib = _lib.load()
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -58,6 +59,14 @@ class Stencil:
         cfg.device = self.device
         cfg.stream = ctypes.c_void_p(self.stream.cuda_stream)
         cfg.flags = _lib.ST_FTZ | (_lib.ST_NO_SWAP if no_swap else 0)
+        # library-owned halo exchange (include/stencil.h st_config.nccl_id): NCCL inside the plan
+        self._nccl_id = None
+        if nccl_id is not None:
+            if len(nccl_id) != _lib.ST_NCCL_ID_BYTES:
+                raise ValueError("nccl_id must be ST_NCCL_ID_BYTES bytes (stencil_nccl_unique_id)")
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), _lib.ST_NCCL_ID_BYTES)
+            cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        self.lib_exchange = nccl_id is not None and nranks > 1
         self._cfg = cfg
         h = ctypes.c_void_p()
         _lib.check(lib.stencil_create(ctypes.byref(cfg), ctypes.byref(h)))
@@ -203,3 +212,11 @@ class Stencil:
 
 def supported(ndim: int, time_order: int, radius: int, t_kernel: int) -> bool:
     return bool(_lib.load().stencil_supported(ndim, time_order, radius, t_kernel))
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (stencil_nccl_unique_id): rank 0 makes it, every rank passes it as
+    Stencil(..., nccl_id=...) to hand the halo exchange to the library."""
+    buf = ctypes.create_string_buffer(_lib.ST_NCCL_ID_BYTES)
+    _lib.check(_lib.load().stencil_nccl_unique_id(buf))
+    return buf.raw

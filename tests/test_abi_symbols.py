@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_host_queries():
     lib = _lib.load()
-    assert lib.stencil_abi_version() == 104
+    assert lib.stencil_abi_version() == 105
     for r in range(1, 9):
         for to in (1, 2):
             assert lib.stencil_supported(3, to, r, 1) == 1
@@ -111,3 +111,16 @@ def test_null_arguments():
 @pytest.mark.parametrize("order", range(2, 17, 2))
 def test_product_fd_weights_equal_oracle(order):
     assert tuple(fornberg_weights(order)) == tuple(oracle.fd_weights_exact(order))
+
+
+def test_nccl_unique_id_host_only():
+    """stencil_nccl_unique_id (library-owned exchange) needs no GPU: the NCCL the process loads
+    (torch's libnccl.so.2) makes the id rank 0 broadcasts."""
+    import torch  # noqa: F401  (loads libnccl.so.2 into the process)
+    lib = _lib.load()
+    buf = ctypes.create_string_buffer(_lib.ST_NCCL_ID_BYTES)
+    st = lib.stencil_nccl_unique_id(buf)
+    if st == _lib.ST_ENCCL:
+        pytest.skip(lib.stencil_last_error(None).decode())
+    assert st == _lib.ST_OK and any(buf.raw)
+    assert lib.stencil_nccl_unique_id(None) == _lib.ST_EINVAL

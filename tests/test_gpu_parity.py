@@ -249,3 +249,17 @@ def test_2d_heat_resident_eigenmode(monkeypatch, resident):
         monkeypatch.setenv("ST_NO_RESIDENT", "1")
     p = W.problem("C1", n=(99, 128, 1), nt=37)
     _check(W.Problem(**dict(p.__dict__, init="eigenmode")))
+
+
+# ----------------------------------------------------------------------------- band/interior split
+@pytest.mark.parametrize("order", [8, 12, 16])
+def test_t1_band_interior_split(monkeypatch, order):
+    """ST_SPLIT_T1: every step as lo band + hi band + interior launches (the split the
+    library-owned NCCL exchange overlaps with the transfer, include/stencil.h), bit-exact, with
+    sources and receivers on band planes."""
+    monkeypatch.setenv("ST_SPLIT_T1", "1")
+    r = order // 2
+    n = (70, 50, 40)
+    src = [(35, 25, 20), (3, 4, r - 1), (66, 45, n[2] - r)]
+    rec = [(10, 10, 0), (20, 30, r), (40, 20, n[2] - 1), (35, 25, n[2] - r - 1)]
+    _check(_wave("C3", n, 9, 5, order=order, src=src, rec=rec))
