@@ -84,12 +84,13 @@ typedef struct {
   uint32_t flags;         /* ST_FTZ (must be set) | ST_NO_SWAP (optional) */
   const void *nccl_id;    /* host ncclUniqueId (ST_NCCL_ID_BYTES bytes, e.g. from
                              stencil_nccl_unique_id on rank 0, broadcast by the caller) or NULL.
-                             With nranks > 1 and nccl_id != NULL the LIBRARY owns the halo
+                             With nccl_id != NULL the LIBRARY owns the halo
                              exchange: stencil_create joins a NCCL communicator (collective: every
                              rank creates its plan concurrently), stencil_run takes any nt, loops
                              over T_c-step periods internally and sums the receiver trace over the
-                             ranks (every rank gets the full trace).  NULL: the caller exchanges
-                             ghost planes between runs of at most t_comm steps. */
+                             ranks (every rank gets the full trace); a one-rank plan runs the same
+                             loop with no neighbours.  NULL: the caller exchanges ghost planes
+                             between runs of at most t_comm steps. */
 } st_config;
 
 #define ST_NCCL_ID_BYTES 128

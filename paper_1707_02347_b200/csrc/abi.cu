@@ -504,8 +504,9 @@ st_status stencil_create(const st_config* cfg, stencil_plan** out) {
   }
   e = cudaEventCreateWithFlags(&p->staging_ev, cudaEventDisableTiming);
   if (e != cudaSuccess) { cuda_fail(p, e, "cudaEventCreate"); return bail(ST_ECUDA); }
-  if (c.nranks > 1 && c.nccl_id) {
-    // library-owned exchange: join the communicator (collective over the ranks)
+  if (c.nccl_id) {
+    // library-owned exchange: join the communicator (collective over the ranks; a one-rank plan
+    // exercises the same time loop, comm stream and trace reduction with no neighbours)
     const NcclApi& api = nccl();
     if (!api.ok) { fail(p, ST_ENCCL, "%s", api.why.c_str()); return bail(ST_ENCCL); }
     ncclUniqueId id;
@@ -1182,12 +1183,13 @@ static st_status run_lib(stencil_plan* p, float* u_prev, float* u_cur, const flo
   if (nrec > 0) CK(cudaMemsetAsync(rec_trace, 0, (size_t)nt * nrec * 4, p->stream), "trace reset");
   float* A = u_prev;   // u^{n-1}
   float* B = u_cur;    // u^n
-  const bool overlap = c.t_comm == 1 && c.t_kernel == 1 && p->nzl >= 2 * r;
+  const bool overlap = c.t_comm <= 1 && c.t_kernel == 1 && p->nzl >= 2 * r;
   const int G = (int)p->G, nzl = (int)p->nzl;
   bool first = true;
   st_status s = ST_OK;
+  const int tc = std::max(1, c.t_comm);
   for (int done = 0; done < nt;) {
-    const int steps = std::min(c.t_comm, nt - done);
+    const int steps = std::min(tc, nt - done);
     const float* v = first ? vel : nullptr;
     const float* d = first ? damp : nullptr;
     float* tr = nrec > 0 ? rec_trace + (size_t)done * nrec : nullptr;

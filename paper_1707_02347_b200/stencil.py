@@ -66,7 +66,7 @@ class Stencil:
                 raise ValueError("nccl_id must be ST_NCCL_ID_BYTES bytes (stencil_nccl_unique_id)")
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), _lib.ST_NCCL_ID_BYTES)
             cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
-        self.lib_exchange = nccl_id is not None and nranks > 1
+        self.lib_exchange = nccl_id is not None
         self._cfg = cfg
         h = ctypes.c_void_p()
         _lib.check(lib.stencil_create(ctypes.byref(cfg), ctypes.byref(h)))

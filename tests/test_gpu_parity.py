@@ -263,3 +263,32 @@ def test_t1_band_interior_split(monkeypatch, order):
     src = [(35, 25, 20), (3, 4, r - 1), (66, 45, n[2] - r)]
     rec = [(10, 10, 0), (20, 30, r), (40, 20, n[2] - 1), (35, 25, n[2] - r - 1)]
     _check(_wave("C3", n, 9, 5, order=order, src=src, rec=rec))
+
+
+# ----------------------------------------------------------------------------- library-owned exchange
+@pytest.mark.parametrize("t_comm,t_kernel", [(1, 1), (3, 1), (4, 2)])
+def test_lib_exchange_single_rank(t_comm, t_kernel):
+    """st_config.nccl_id on a one-rank plan: the library-owned time loop (T_c periods, NCCL group
+    calls with no neighbours, comm-stream joins, trace zeroing and ncclAllReduce) runs for real on
+    one GPU and stays bit-exact; the multi-rank transfers need >= 2 GPUs."""
+    import torch
+    from paper_1707_02347_b200 import Stencil
+    from paper_1707_02347_b200.stencil import nccl_unique_id
+    p = _wave("C3", (60, 44, 36), 11, 5, src=[(30, 22, 18)], rec=[(30, 22, 18), (5, 40, 2), (59, 0, 35)])
+    st = Stencil(p.ndim, p.n, p.space_order, p.time_order, p.dt, p.dx, t_kernel=t_kernel,
+                 t_comm=t_comm, nccl_id=nccl_unique_id())
+    assert st.lib_exchange
+    up, uc = W.initial_fields(p)
+    P = st.embed(torch.from_numpy(up).cuda())
+    C = st.embed(torch.from_numpy(uc).cuda())
+    vel = st.embed(torch.from_numpy(W.velocity(p)).cuda())
+    damp = st.embed(torch.from_numpy(W.damp(p)).cuda())
+    wav = torch.from_numpy(W.wavelet(p, p.nt)).cuda()
+    trace = torch.full((p.nt, len(p.rec)), float("nan"), device="cuda")   # the library zeroes it
+    st.run(P, C, p.nt, vel=vel, damp=damp, src=list(p.src), wavelet=wav, rec=list(p.rec), trace=trace)
+    st.sync()
+    op, oc, ot = oracle_run(p)
+    assert np.array_equal(st.interior(C).cpu().numpy(), oc)
+    assert np.array_equal(st.interior(P).cpu().numpy(), op)
+    assert np.array_equal(trace.cpu().numpy(), ot)
+    st.close()
