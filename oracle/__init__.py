@@ -13,6 +13,8 @@ Contents
   run_untiled(...)         O1, the plain untiled loop nest.
   run_literal(...)         O1-literal: the paper's printed wave expression and term order
                            (P:1678-1708), to bound fp32 order drift (reading Q8).
+  run_slabs(...)           O3: the GPU's z-slab schedule (ghost depth r*T_c, exchange every T_c
+                           steps, shrinking redundant regions), plain loops; bitwise O1.
   run_skewed(...)          O2, the paper's skewed time-tiled schedule.
   embed/extract            oracle layout <-> interior arrays.
 
@@ -65,6 +67,8 @@ def _load():
             f = getattr(lib, nm)
             f.argtypes = common + [I, I, I, I, I]
             f.restype = I
+        lib.oracle_run_slabs_f32.argtypes = common + [I, I, I]
+        lib.oracle_run_slabs_f32.restype = I
         for nm in ("oracle_run_literal_f32", "oracle_run_literal_f64"):
             f = getattr(lib, nm)
             f.argtypes = [I, L, L, L, I, P, P, D, P, P, P, P, I, L, I, P, P, I, P, P, I]
@@ -197,6 +201,35 @@ def run_skewed(ndim, n, order, coeffs, h, time_order, dt, P, C, a=None, c=None, 
                 src, wavelet, rec, ftz, extra=(Tt, Tz, Ty, B, skew))
 
 
+def run_slabs(ndim, n, order, coeffs, h, time_order, dt, P, C, a=None, c=None, nt=1, step0=0,
+              src=(), wavelet=None, rec=(), ftz=True, nslab=2, tc=1, ghost=None):
+    """O3: the GPU's z-slab schedule emulated with plain loops (oracle.cpp run_slabs): nslab slabs,
+    ghost planes (default radius*tc) refreshed every tc steps, shrinking redundant regions.
+    fp32 only.  Equals O1 bit for bit when ghost >= radius*tc."""
+    assert P.dtype == np.float32
+    ghost = (order // 2) * tc if ghost is None else ghost
+    dtype = P.dtype
+    r = order // 2
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    src, rec = list(src or []), list(rec or [])
+    src_a, rec_a = _pts(src), _pts(rec)
+    if src:
+        wavelet = np.ascontiguousarray(wavelet, dtype=dtype)
+    trace = np.zeros((nt, max(len(rec), 1)), dtype=dtype)
+    if time_order == 2:
+        a = np.ascontiguousarray(a, dtype=dtype)
+        c = np.ascontiguousarray(c, dtype=dtype)
+    rc = _load().oracle_run_slabs_f32(ndim, n[0], n[1], n[2], r, _ptr(coeffs), _ptr(h), time_order,
+                                      float(dt), _ptr(P), _ptr(C), _ptr(a) if time_order == 2 else None,
+                                      _ptr(c) if time_order == 2 else None, nt, step0, len(src),
+                                      _ptr(src_a), _ptr(wavelet) if src else None, len(rec), _ptr(rec_a),
+                                      _ptr(trace), int(ftz), nslab, tc, ghost)
+    if rc != 0:
+        raise ValueError(f"oracle_run_slabs rejected its arguments (rc={rc})")
+    return trace[:, :len(rec)]
+
+
 def run_literal(ndim, n, order, coeffs, h, dt, P, C, vel, damp, nt=1, step0=0, src=(), wavelet=None,
                 rec=(), ftz=True):
     """O1-literal: the wave update in the paper's printed expression and term order
@@ -237,6 +270,11 @@ def run_problem(p, nt=None, dtype=np.float32, kind="untiled", ftz=True, **kw):
         dmp = embed(W.damp(p), p.ndim, r, dtype)
         a, c = medium(vel, dmp, p.dt, dtype=dtype, ftz=ftz)
     wv = W.wavelet(p, nt).astype(dtype) if p.src else None
+    if kind == "slabs":
+        h = p.dx[:p.ndim] if p.ndim == 3 else p.dx[:2]
+        tr = run_slabs(p.ndim, p.n, p.space_order, fd_weights(p.space_order), h, p.time_order, p.dt, P, C,
+                       a, c, nt, 0, list(p.src), wv, list(p.rec), ftz, **kw)
+        return extract(P, p.ndim, p.n, r), extract(C, p.ndim, p.n, r), tr
     if kind == "literal":
         assert p.time_order == 2
         vel = embed(W.velocity(p), p.ndim, r, dtype)

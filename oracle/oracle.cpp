@@ -27,6 +27,9 @@
 //                      expression and term order, fp32: bounds the drift of the
 //                      canonical order against the paper's own (reading Q8); not the reference.
 //
+//  * O3 oracle_run_slabs_*  emulation of the GPU's z-slab schedule (ghost zones of depth r*T_c,
+//                      exchange every T_c steps, shrinking redundant regions): bitwise O1.
+//
 //  * O2 oracle_run_skewed_*    the paper's time-tiled schedule:
 //                      loop order tt, zz, yy, t, z', y', x with the tiled
 //                      (slow) axes skewed by `skew`*t (P:1196-1202, P:1445
@@ -333,6 +336,128 @@ int run_skewed(int ndim, long nx, long ny, long nz, int r, const double* coeffs,
   return 0;
 }
 
+// ---------------------------------------------------------------------------- O3
+// Emulation of the GPU's z-slab schedule, plain loops:
+// the interior planes are split into S slabs; each slab keeps its own copy of the fields with
+// `ghost` extra planes per side (zero at the global boundary); every T_c steps the slabs copy their
+// neighbours' owned planes into their ghost zones (depth r*T_c of u^n and r*(T_c-1) of u^{n-1},
+// what the library exchanges), then advance T_c steps without communication over regions that
+// shrink by r per step (ghost planes are computed redundantly, sources injected there too),
+// receivers sampled by the owning slab only.  Must equal O1 bit for bit whenever ghost >= r*T_c;
+// a shallower ghost zone must not (negative control).
+template <class T>
+int run_slabs(int ndim, long nx, long ny, long nz, int r, const double* coeffs, const double* h,
+              int time_order, double dt, T* P, T* C, const T* a, const T* c, int nt, long step0,
+              int nsrc, const int64_t* src_xyz, const T* wavelet, int nrec, const int64_t* rec_xyz,
+              T* trace, int ftz, int nslab, int tc, int ghost) {
+  if (ndim != 3 || nslab < 1 || tc < 1 || ghost < 0 || nz % nslab) return 1;
+  const Geo g(ndim, nx, ny, nz, r);           // the global arrays (oracle layout, halo r)
+  const Coef<T> cf = make_coef<T>(g, coeffs, h);
+  const T dtT = (T)dt;
+  const long nzl = nz / nslab;
+  const long sz = g.sz;
+  FtzGuard guard(ftz);
+  // slab s stores global planes [z0 - gl, z0 + nzl + gh) at local planes [0, ...), plus the
+  // r-plane halo the per-point update reads beyond them (always zero)
+  struct Slab { long z0, gl, gh, nloc; std::vector<T> P, C, A, Cc; };
+  std::vector<Slab> sl(nslab);
+  for (int s = 0; s < nslab; ++s) {
+    Slab& b = sl[s];
+    b.z0 = s * nzl;
+    b.gl = s > 0 ? ghost : 0;
+    b.gh = s < nslab - 1 ? ghost : 0;
+    b.nloc = b.gl + nzl + b.gh;
+    const long tot = (b.nloc + 2 * r) * sz;
+    b.P.assign(tot, (T)0); b.C.assign(tot, (T)0);
+    if (time_order == 2) { b.A.assign(tot, (T)0); b.Cc.assign(tot, (T)0); }
+    for (long lz = 0; lz < b.nloc; ++lz) {      // state on owned planes; medium on every plane
+      const long gz = b.z0 - b.gl + lz;
+      for (long i = 0; i < sz; ++i) {
+        const long src = (gz + r) * sz + i, dst = (lz + r) * sz + i;
+        if (lz >= b.gl && lz < b.gl + nzl) { b.P[dst] = P[src]; b.C[dst] = C[src]; }
+        if (time_order == 2) { b.A[dst] = a[src]; b.Cc[dst] = c[src]; }
+      }
+    }
+  }
+  // a slab-local geometry: same x/y, nloc planes
+  auto local_idx = [&](long x, long y, long lz) { return (lz + r) * sz + (y + r) * g.sy + (x + r); };
+  const PointList S = make_points(g, nsrc, src_xyz);
+  for (long done = 0; done < nt;) {
+    const long steps = std::min<long>(tc, nt - done);
+    // exchange: ghost planes from the neighbours' owned planes (u^n depth r*steps, u^{n-1} r*(steps-1))
+    for (int s = 0; s < nslab; ++s) {
+      Slab& b = sl[s];
+      const long dc = std::min<long>(r * steps, ghost), dp = std::min<long>(r * (steps - 1), ghost);
+      for (int side = 0; side < 2; ++side) {
+        if ((side == 0 && s == 0) || (side == 1 && s == nslab - 1)) continue;
+        const Slab& nb = sl[side == 0 ? s - 1 : s + 1];
+        for (int f = 0; f < 2; ++f) {
+          const long d = f == 0 ? dc : dp;
+          for (long k = 0; k < d; ++k) {
+            // my ghost plane and the global plane it mirrors
+            const long lz = side == 0 ? b.gl - 1 - k : b.gl + nzl + k;
+            const long gz = b.z0 - b.gl + lz;
+            const long nlz = gz - (nb.z0 - nb.gl);
+            const std::vector<T>& from = f == 0 ? nb.C : nb.P;
+            std::vector<T>& to = f == 0 ? b.C : b.P;
+            std::copy(from.begin() + (nlz + r) * sz, from.begin() + (nlz + r + 1) * sz, to.begin() + (lz + r) * sz);
+          }
+        }
+      }
+    }
+    for (long j = 0; j < steps; ++j) {
+      const long n = done + j;
+      const T* w_step = nsrc ? wavelet + (step0 + n) * nsrc : nullptr;
+      for (int s = 0; s < nslab; ++s) {
+        Slab& b = sl[s];
+        const long ext = (long)r * (steps - 1 - j);
+        const long lo = b.gl - (s > 0 ? std::min(ext, b.gl) : 0);
+        const long hi = b.gl + nzl + (s < nslab - 1 ? std::min(ext, b.gh) : 0);
+        // the per-point update reads u^n at lz +- r; a slab-local Geo view of the arrays
+        Geo lg(3, nx, ny, b.nloc, r);
+        for (long lz = lo; lz < hi; ++lz) {
+          const long gz = b.z0 - b.gl + lz;
+          for (long y = 0; y < ny; ++y) {
+            const bool hs = nsrc && row_has_source<T>(S, y, gz);
+            for (long x = 0; x < nx; ++x) {
+              const long pl = local_idx(x, y, lz);
+              // sources by global position: a one-source list per matching point
+              T acc_unused = 0; (void)acc_unused;
+              PointList Sl;
+              if (hs)
+                for (size_t q = 0; q < S.p.size(); ++q) {
+                  Sl.p.push_back(S.p[q] == g.idx(x, y, gz) ? pl : -1);
+                  Sl.y.push_back(S.y[q]); Sl.z.push_back(S.z[q]);
+                }
+              b.P[pl] = update_point<T>(lg, cf, time_order, dtT, b.C.data(), b.P.data(),
+                                        time_order == 2 ? b.A.data() : nullptr,
+                                        time_order == 2 ? b.Cc.data() : nullptr, pl, Sl, w_step, y, gz, hs);
+            }
+          }
+        }
+      }
+      for (int k = 0; k < nrec; ++k) {           // owner-only receivers
+        const long gz = rec_xyz[3 * k + 2];
+        const int s = (int)(gz / nzl);
+        const Slab& b = sl[s];
+        trace[(long)n * nrec + k] = b.P[local_idx(rec_xyz[3 * k], rec_xyz[3 * k + 1], gz - b.z0 + b.gl)];
+      }
+      for (int s = 0; s < nslab; ++s) std::swap(sl[s].P, sl[s].C);
+    }
+    done += steps;
+  }
+  // gather the owned planes; (u_prev, u_cur) = (u^{n+nt-1}, u^{n+nt})
+  for (int s = 0; s < nslab; ++s) {
+    const Slab& b = sl[s];
+    for (long lz = b.gl; lz < b.gl + nzl; ++lz) {
+      const long gz = b.z0 - b.gl + lz;
+      std::copy(b.P.begin() + (lz + r) * sz, b.P.begin() + (lz + r + 1) * sz, P + (gz + r) * sz);
+      std::copy(b.C.begin() + (lz + r) * sz, b.C.begin() + (lz + r + 1) * sz, C + (gz + r) * sz);
+    }
+  }
+  return 0;
+}
+
 template <class T>
 void medium(long npts, const T* vel, const T* eta, double dt, T* a, T* c, int ftz) {
   const T dtT = (T)dt;
@@ -391,6 +516,15 @@ int oracle_run_literal_f64(int ndim, long nx, long ny, long nz, int r, const dou
                            int ftz) {
   return run_literal<double>(ndim, nx, ny, nz, r, coeffs, h, dt, P, C, vel, damp, nt, step0, nsrc,
                              src_xyz, wavelet, nrec, rec_xyz, trace, ftz);
+}
+
+int oracle_run_slabs_f32(int ndim, long nx, long ny, long nz, int r, const double* coeffs,
+                         const double* h, int time_order, double dt, float* P, float* C,
+                         const float* a, const float* c, int nt, long step0, int nsrc,
+                         const int64_t* src_xyz, const float* wavelet, int nrec,
+                         const int64_t* rec_xyz, float* trace, int ftz, int nslab, int tc, int ghost) {
+  return run_slabs<float>(ndim, nx, ny, nz, r, coeffs, h, time_order, dt, P, C, a, c, nt, step0, nsrc,
+                          src_xyz, wavelet, nrec, rec_xyz, trace, ftz, nslab, tc, ghost);
 }
 
 int oracle_run_skewed_f32(int ndim, long nx, long ny, long nz, int r, const double* coeffs,

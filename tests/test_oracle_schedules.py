@@ -84,3 +84,33 @@ def test_run_composition_bitwise():
                             src=p.src, wavelet=wv, rec=p.rec)
     assert np.array_equal(C, C2) and np.array_equal(P, P2)
     assert np.array_equal(np.concatenate([ta, tb]), tt)
+
+
+# ----------------------------------------------------------------------------- O3: z-slab schedule
+@pytest.mark.parametrize("time_order,order", [(2, 8), (2, 4), (1, 2)])
+@pytest.mark.parametrize("nslab,tc", [(2, 1), (3, 2), (4, 3), (2, 4)])
+def test_slab_schedule_equals_untiled(time_order, order, nslab, tc):
+    """O3 (the library's z-slab decomposition: ghost planes r*T_c of u^n and r*(T_c-1) of u^{n-1}
+    refreshed every T_c steps, redundant shrinking regions, sources injected in ghost planes too,
+    owner-only receivers) reproduces O1 bit for bit (S:458 pattern)."""
+    r = order // 2
+    nz = nslab * max(4, r * tc)
+    if time_order == 2:
+        p = W.problem("C3", n=(14, 12, nz), nt=11, sponge=2)
+        p = W.Problem(**{**p.__dict__, "space_order": order,
+                         "src": ((7, 6, nz // nslab - 1), (3, 2, nz // 2)),
+                         "rec": ((7, 6, nz // nslab), (1, 1, 0), (13, 11, nz - 1))})
+    else:
+        p = W.problem("C2", n=(13, 11, nz), nt=9)
+    want = oracle.run_problem(p)
+    got = oracle.run_problem(p, kind="slabs", nslab=nslab, tc=tc)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_slab_schedule_shallow_ghost_differs():
+    """Negative control: a ghost zone one plane shallower than r*T_c changes the result."""
+    p = W.problem("C2", n=(13, 11, 24), nt=9)
+    want = oracle.run_problem(p)
+    got = oracle.run_problem(p, kind="slabs", nslab=3, tc=3, ghost=2)
+    assert not np.array_equal(got[1], want[1])
