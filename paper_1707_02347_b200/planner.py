@@ -70,15 +70,14 @@ class Plan:
     reason: str
 
 
-# Measured on B200 (512^3 x 200 steps unless noted): GPts/s of the untiled and the
-# two-level kernels; 0 = not compiled as the warp-group kernel / not measured.
+# Measured on B200 (profiles/r02/study_tiling_vs_order.jsonl: 512^3, wave 200 steps,
+# heat 100 steps, one box): GPts/s of the untiled kernel and of the T_k = 2 pass that build.py
+# compiles for the shape (wave r <= 2: overlapped tiles sweep2; r >= 3: the L1/L2 exchange pass
+# sweepx; heat: sweep2).
 _MEASURED = {  # (time_order, radius): (T=1, T_k=2)
-    (2, 1): (332, 423), (2, 2): (330, 378), (2, 3): (316, 266), (2, 4): (318, 226),
-    (2, 5): (300, 0),   # between SO8 and SO12 (estimate)
-    (2, 6): (285, 0),   # C5 768^3 x 2000 (bench, sweep1s)
-    (2, 7): (256, 0),   # SO14 study run
-    (2, 8): (254, 0),   # C4 1024^3 x 1000 (bench, sweep1s ISO)
-    (1, 1): (708, 677), (1, 2): (700, 0),
+    (2, 1): (334.5, 424.8), (2, 2): (332.7, 380.0), (2, 3): (321.7, 264.1), (2, 4): (319.6, 250.4),
+    (2, 5): (326.2, 228.8), (2, 6): (318.7, 205.9), (2, 7): (264.8, 178.4), (2, 8): (247.5, 118.2),
+    (1, 1): (742.9, 681.2),
 }
 NVLINK_GBS = 770.0          # measured peer copy per direction (B200_PROFILING.md)
 EXCHANGE_LATENCY_US = 25.0  # NCCL send/recv launch + sync per exchange (estimate)
@@ -95,7 +94,8 @@ def plan(time_order: int, radius: int, n: Sequence[int], nranks: int = 1, ndim: 
     t1, t2 = _MEASURED.get((time_order, radius), (1.0, 0.0))
     tk = 2 if (ndim == 3 and t2 > t1 and ok(2)) else 1
     why = (f"T_k=2 measured {t2} vs T=1 {t1} GPts/s" if tk == 2 else
-           f"T=1 (untiled kernel at the HBM roofline; T_k=2 measured {t2 or 'n/a'} GPts/s)")
+           f"T=1 (measured {t1} vs T_k=2 {t2} GPts/s on 512^3)" if t2 else
+           "T=1 (no T_k=2 measurement for this shape)")
     tc = tk
     if nranks > 1:
         nx, ny, nz = n
