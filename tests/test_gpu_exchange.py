@@ -1,9 +1,10 @@
-"""GPU parity of the exchange-tiled T_k = 2 kernel (sweept.cuh) against the CPU oracle, bit for
-bit, on shapes that force its scheduling corner cases: band cuts (ST_EXCH_SLOTS caps the tiles a
-band may hold, so small grids get many bands, down to one tile row per band), several z-chunks
-(ST_EXCH_CHUNKS), ragged x/y/z extents, sources and receivers on band-cut rows and chunk-boundary
-planes, odd step counts (a final T = 1 pass), and repeated runs of one plan (progress counters and
-ticket carried across launches)."""
+"""GPU parity of the time-tiled T_k = 2 exchange pass (sweepx.cuh: L1 tiles compute u^{n+1} and
+publish per-plane progress, L2 tiles on the grid skewed r rows up compute u^{n+2} from the L1
+tiles' stores) against the CPU oracle, bit for bit, on shapes that force its scheduling corner
+cases: several z-chunks (ST_EXCH_CHUNKS; a chunk's L1 tiles also compute the r planes on each
+side), ragged x/y/z extents, sources and receivers on tile-row boundaries and on the skewed L2 rows
+and chunk-boundary planes, odd step counts (a final T = 1 pass), and repeated runs of one plan
+(progress words and ticket carried across launches)."""
 from __future__ import annotations
 
 import numpy as np
@@ -32,37 +33,28 @@ def _same(p, **kw):
     assert np.array_equal(gt, ot), "receiver traces differ"
 
 
-@pytest.mark.parametrize("order,n,nt,slots,chunks", [
-    (2, (70, 50, 20), 9, 2, 4),
-    (4, (96, 61, 31), 8, 3, 2),
-    (8, (150, 100, 40), 9, 6, 3),
-    (8, (150, 100, 40), 10, 1000, 1),
-    (12, (130, 90, 33), 7, 3, 2),
-    (12, (130, 90, 33), 6, 4, 1),
-    (14, (100, 70, 36), 5, 2, 2),
+@pytest.mark.parametrize("order,n,nt,chunks", [
+    (6, (96, 61, 31), 8, 2),
+    (8, (150, 100, 40), 9, 3),
+    (8, (150, 100, 40), 10, 1),
+    (12, (130, 90, 33), 7, 2),
+    (12, (130, 90, 33), 6, 1),
+    (14, (100, 70, 36), 5, 2),
+    (16, (70, 52, 34), 5, 3),
 ])
-def test_exchange_bands_chunks(monkeypatch, order, n, nt, slots, chunks):
-    monkeypatch.setenv("ST_EXCH_SLOTS", str(slots))
+def test_exchange_chunks_and_edges(monkeypatch, order, n, nt, chunks):
     monkeypatch.setenv("ST_EXCH_CHUNKS", str(chunks))
     r = order // 2
     nx, ny, nz = n
-    # sources / receivers on rows and planes next to tile-row, band and chunk boundaries
-    zc = (nz + chunks - 1) // chunks          # first plane of the second chunk
-    zc = min(zc, nz - 1)
-    src = [(nx // 2, ny // 2, nz // 2), (1, 14 - r, zc), (nx - 2, 13, 2)]
-    rec = [(nx // 2, 14, nz // 2), (3, 14 - r - 1, zc - 1), (nx - 1, ny - 1, nz - 1),
-           (0, 27, 1), (63, 28, nz // 2), (64, 14 + 14 - r, 5)]
+    zc = min((nz + chunks - 1) // chunks, nz - 1)     # first plane of the second chunk
+    # rows at L1 tile-row edges (multiples of 16 and 24) and at the skewed L2 edges (minus r)
+    src = [(nx // 2, ny // 2, nz // 2), (1, 24 - r, zc), (nx - 2, 16, 2)]
+    rec = [(nx // 2, 24, nz // 2), (3, 24 - r - 1, zc - 1), (nx - 1, ny - 1, nz - 1),
+           (0, 16 - r, 1), (63, 48 - r, nz // 2), (64, 47, 5)]
     _same(_wave(n, nt, order, src=src, rec=rec))
 
 
-def test_exchange_heat_bands(monkeypatch):
-    monkeypatch.setenv("ST_EXCH_SLOTS", "5")
-    monkeypatch.setenv("ST_EXCH_CHUNKS", "3")
-    _same(W.problem("C2", n=(131, 70, 45), nt=11))
-
-
-def test_exchange_repeated_runs(monkeypatch):
+def test_exchange_repeated_runs():
     """One plan, several runs: the ticket and progress words carry over between launches."""
-    monkeypatch.setenv("ST_EXCH_SLOTS", "4")
     p = _wave((90, 60, 30), 12, 8, rec=[(45, 30, 15), (2, 10, 3)])
     _same(p, splits=[4, 2, 6])
