@@ -100,7 +100,9 @@ def instances():
             out.append((2, wave, R, 1, vy, ncw, 1))
         out.append((2, wave, 1, 2) + _vy_nwy(2, 1, 2) + (0,))
         out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4) + (0,))
-    for R, TK in ((1, 4), (2, 4), (1, 8)):
+    # heat T_k = 4 (sweep2); T_k = 8 (first-generation kernel, 46 GPts/s on 512^3 vs 708 at T = 1)
+    # is retired: stencil_create reports ST_EUNSUPPORTED for it
+    for R, TK in ((1, 4), (2, 4)):
         oy = _sweep2_oy(0, R, TK)
         out.append((3, 0, R, TK, 2, oy, 2) if oy else (3, 0, R, TK) + _vy_nwy(3, R, TK) + (0,))
     return out

@@ -48,7 +48,7 @@ def test_C1_heat2d_full(tk):
     _check(W.problem("C1"), t_kernel=tk)
 
 
-@pytest.mark.parametrize("tk", [1, 2, 4, 8])
+@pytest.mark.parametrize("tk", [1, 2, 4])
 def test_heat3d_ragged(tk):
     _check(W.problem("C2", n=(131, 70, 45), nt=13), t_kernel=tk)
 
