@@ -662,6 +662,7 @@ static st_status upload_tables(stencil_plan* p, int32_t nsrc, const int32_t* src
 }
 
 static int choose_chunks(const stencil_plan* p, const st::KernelEntry* k, int bps, long long tiles, long long planes) {
+  if (const char* e = getenv("ST_CHUNKS")) return std::max(1, atoi(e));   // tuning override
   const long long slots = (long long)p->sm_count * std::max(1, bps);
   double best = 1e300;
   int bestc = 1;
@@ -673,6 +674,14 @@ static int choose_chunks(const stencil_plan* p, const st::KernelEntry* k, int bp
     const double per = (double)chunk + 2.0 * k->rz * k->tk;   // warm-up + redundant levels
     const double t = waves * per;
     if (t < best * 0.999) { best = t; bestc = c; }
+  }
+  // static-ring instances (r = 5, 6, 8) measured faster with >= ~16 waves of shorter chunks than
+  // the model above predicts (C5: 3 chunks 273.5, 6 chunks 280.1-280.6, 8 chunks 281.4-281.7
+  // GPts/s, same box; C4 unchanged at 2-4 chunks): split further while chunks stay >= 8r planes
+  if (k->fixed_slots > 0 && k->tk == 1) {
+    while (bestc < 32 && (tiles * bestc + slots - 1) / slots < 16 &&
+           (planes + bestc) / (bestc + 1) >= 8LL * k->rz)
+      ++bestc;
   }
   return bestc;
 }
