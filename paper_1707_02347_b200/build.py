@@ -80,6 +80,15 @@ def _exch(wave: int, R: int) -> bool:
     return bool(wave) and R >= 3
 
 
+HEAT_H = (4, 16)   # (rows per warp, warps) of the register-resident heat time-tiled kernel (kind 5)
+
+
+def _heat_h(R: int, TK: int) -> bool:
+    """Heat T_k > 1 instances built as sweeph (kind 5: every level in one warp's registers, x
+    neighbours by SHFL, one CTA barrier per step; DESIGN.md §6 G5)."""
+    return R == 1 and TK in (2, 3, 4)
+
+
 def instances():
     """(ndim, wave, R, TK, VY, NWY, kind) compiled into this build.
     For kind 2 the NWY slot holds the output rows OY of the instance."""
@@ -89,7 +98,9 @@ def instances():
             ncw, vy = _t1_geom(3, wave, R)
             out.append((3, wave, R, 1, vy, ncw, 3 if _static_ring(3, wave, R) else 1))
             oy = _sweep2_oy(wave, R, 2)
-            if _exch(wave, R):
+            if not wave and _heat_h(R, 2):
+                out.append((3, 0, R, 2) + HEAT_H + (5,))
+            elif _exch(wave, R):
                 out.append((3, wave, R, 2, vy, ncw, 4))        # L1/L2 roles, untiled geometry
             elif oy:
                 out.append((3, wave, R, 2, 2, oy, 2))
@@ -102,7 +113,11 @@ def instances():
         out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4) + (0,))
     # heat T_k = 4 (sweep2); T_k = 8 (first-generation kernel, 46 GPts/s on 512^3 vs 708 at T = 1)
     # is retired: stencil_create reports ST_EUNSUPPORTED for it
+    out.append((3, 0, 1, 3) + HEAT_H + (5,))
     for R, TK in ((1, 4), (2, 4)):
+        if _heat_h(R, TK):
+            out.append((3, 0, R, TK) + HEAT_H + (5,))
+            continue
         oy = _sweep2_oy(0, R, TK)
         out.append((3, 0, R, TK, 2, oy, 2) if oy else (3, 0, R, TK) + _vy_nwy(3, R, TK) + (0,))
     return out
@@ -126,6 +141,8 @@ def _gen_sources(groups: int, inst=None, outdir: str = BUILD):
                 lines.append(f"  make_entry2<{R}, {TK}, {w}, {NWY}>(),")   # NWY = output rows
             elif kind == 4:
                 lines.append(f"  make_entryX<{R}, {w}, {NWY}, {VY}>(),")
+            elif kind == 5:
+                lines.append(f"  make_entryH<{R}, {TK}, {VY}, {NWY}>(),")
             else:
                 lines.append(f"  make_entry<{R}, {TK}, {w}, {ndim}, {VY}, {NWY}>(),")
         lines += ["};", f"extern const int kInst{gi}Count = {len(group)};", "}  // namespace st", ""]

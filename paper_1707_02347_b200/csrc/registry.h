@@ -10,6 +10,7 @@
 #include "sweep1s.cuh"
 #include "sweep2.cuh"
 #include "sweepx.cuh"
+#include "sweeph.cuh"
 
 #ifndef ST_T1_DEPTH
 #define ST_T1_DEPTH 6   // untiled kernel: ring planes of prefetch beyond the radius+1 in use
@@ -263,6 +264,48 @@ constexpr KernelEntry make_entryX() {
                 &launch_sweepx<R, WAVE, NCW, VY>, &query_sweepx<R, WAVE, NCW, VY>, ST_T1_DEPTH};
   e.exch = 1;
   return e;
+}
+
+// ---- time-tiled heat sweep with every level in one warp's registers (sweeph.cuh, G5)
+template <int R, int TK, int VY, int NW>
+cudaError_t launch_sweeph(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
+                          size_t smem, cudaStream_t stream) {
+  const int block = 32 * NW;
+  const bool ev = p.wavelet != nullptr || p.trace != nullptr;   // sources / receivers in this run
+  if (p.outS) {
+    if (ev) return launch_pdl(sweeph_kernel<R, TK, VY, NW, 3>, grid, block, smem, stream, maps.u, p, nslot);
+    return launch_pdl(sweeph_kernel<R, TK, VY, NW, 1>, grid, block, smem, stream, maps.u, p, nslot);
+  }
+  if (ev) return launch_pdl(sweeph_kernel<R, TK, VY, NW, 2>, grid, block, smem, stream, maps.u, p, nslot);
+  return launch_pdl(sweeph_kernel<R, TK, VY, NW, 0>, grid, block, smem, stream, maps.u, p, nslot);
+}
+
+template <int R, int TK, int VY, int NW>
+cudaError_t query_sweeph(size_t smem, cudaFuncAttributes* attr, int* bps, int nthreads) {
+  auto k = sweeph_kernel<R, TK, VY, NW, 0>;
+  cudaError_t e = cudaSuccess;
+  for (auto kk : {k, sweeph_kernel<R, TK, VY, NW, 1>, sweeph_kernel<R, TK, VY, NW, 2>, sweeph_kernel<R, TK, VY, NW, 3>}) {
+    e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if (attr) {
+    e = cudaFuncGetAttributes(attr, k);
+    if (e != cudaSuccess) return e;
+  }
+  if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, nthreads, smem);
+  return cudaSuccess;
+}
+
+#ifndef ST_TH_DEPTH
+#define ST_TH_DEPTH 4   // heat time-tiled kernel: ring planes of prefetch beyond the radius+1 in use
+#endif
+
+template <int R, int TK, int VY, int NW>
+constexpr KernelEntry make_entryH() {
+  using G = GeomH<R, TK, VY, NW>;
+  return KernelEntry{3, 1, R, TK, VY, NW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+                     R, (size_t)G::SLOT_BYTES, (size_t)G::FIXED_BYTES,
+                     &launch_sweeph<R, TK, VY, NW>, &query_sweeph<R, TK, VY, NW>, ST_TH_DEPTH};
 }
 
 }  // namespace st

@@ -16,11 +16,12 @@ def main():
     ap.add_argument("--tk", type=int, default=1)
     ap.add_argument("--nt", type=int, default=6)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--grid", default=None, help="interior grid override, e.g. 512x512x512")
     a = ap.parse_args()
     import torch
     import workloads as W
     from paper_1707_02347_b200.dist import SlabRunner
-    p = W.problem(a.config)
+    p = W.problem(a.config, n=tuple(int(v) for v in a.grid.split("x")) if a.grid else None)
     r = SlabRunner(p, t_kernel=a.tk, device=0)
     host = r.host_inputs(a.nt, pin=False)
     dev = r.to_device(host)
