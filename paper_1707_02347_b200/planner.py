@@ -70,14 +70,19 @@ class Plan:
     reason: str
 
 
-# Measured on B200 (profiles/r02/study_tiling_vs_order.jsonl: 512^3, wave 200 steps,
-# heat 100 steps, one box): GPts/s of the untiled kernel and of the T_k = 2 pass that build.py
-# compiles for the shape (wave r <= 2: overlapped tiles sweep2; r >= 3: the L1/L2 exchange pass
-# sweepx; heat: sweep2).
-_MEASURED = {  # (time_order, radius): (T=1, T_k=2)
-    (2, 1): (334.5, 424.8), (2, 2): (332.7, 380.0), (2, 3): (321.7, 264.1), (2, 4): (319.6, 250.4),
-    (2, 5): (326.2, 228.8), (2, 6): (318.7, 205.9), (2, 7): (264.8, 178.4), (2, 8): (247.5, 118.2),
-    (1, 1): (742.9, 681.2),
+# Measured on B200 (profiles/r02/study_tiling_vs_order.jsonl and
+# profiles/r02/heat_tiling.txt: 512^3, wave 200 steps, heat 96 steps, one box): GPts/s per T_k of
+# the instance build.py compiles for the shape (wave T_k = 2: r <= 2 overlapped tiles sweep2,
+# r >= 3 the L1/L2 exchange pass sweepx; heat T_k = 2..4: the register-resident sweeph).
+_MEASURED = {  # (time_order, radius): {T_k: GPts/s}
+    (2, 1): {1: 334.5, 2: 424.8}, (2, 2): {1: 332.7, 2: 380.0}, (2, 3): {1: 321.7, 2: 264.1},
+    (2, 4): {1: 319.6, 2: 250.4}, (2, 5): {1: 326.2, 2: 228.8}, (2, 6): {1: 318.7, 2: 205.9},
+    (2, 7): {1: 264.8, 2: 178.4}, (2, 8): {1: 247.5, 2: 118.2},
+    (1, 1): {1: 745.8, 2: 1126.4, 3: 1155.8, 4: 1081.4},
+}
+# grids whose own measurement differs from the 512^3 ranking (tile raggedness, L2 residency)
+_MEASURED_GRID = {
+    (1, 1, (256, 256, 256)): {1: 635.3, 2: 737.6, 3: 819.4, 4: 889.2},   # C2
 }
 NVLINK_GBS = 770.0          # measured peer copy per direction (B200_PROFILING.md)
 EXCHANGE_LATENCY_US = 25.0  # NCCL send/recv launch + sync per exchange (estimate)
@@ -91,16 +96,21 @@ def plan(time_order: int, radius: int, n: Sequence[int], nranks: int = 1, ndim: 
     skewed = skew(deps, f)
     assert band_permutable(skewed, [0, 1, 2, 3]) and f[3 if ndim == 2 else 1] == radius
     ok = supported or (lambda tk: True)
-    t1, t2 = _MEASURED.get((time_order, radius), (1.0, 0.0))
-    tk = 2 if (ndim == 3 and t2 > t1 and ok(2)) else 1
-    why = (f"T_k=2 measured {t2} vs T=1 {t1} GPts/s" if tk == 2 else
-           f"T=1 (measured {t1} vs T_k=2 {t2} GPts/s on 512^3)" if t2 else
-           "T=1 (no T_k=2 measurement for this shape)")
+    rates = _MEASURED_GRID.get((time_order, radius, tuple(n)), _MEASURED.get((time_order, radius), {}))
+    t1 = rates.get(1, 1.0)
+    cands = [k for k in sorted(rates) if k > 1 and ndim == 3 and ok(k)]
+    tk = max(cands, key=lambda k: rates[k], default=1)
+    if tk > 1 and rates[tk] <= t1:
+        tk = 1
+    others = ", ".join(f"T_k={k} {rates[k]}" for k in sorted(rates) if k > 1)
+    why = (f"T_k={tk} measured {rates[tk]} vs T=1 {t1} GPts/s" if tk > 1 else
+           f"T=1 (measured {t1} vs {others} GPts/s)" if others else
+           "T=1 (no T_k > 1 measurement for this shape)")
     tc = tk
     if nranks > 1:
         nx, ny, nz = n
         nzl = nz // nranks
-        rate = 1e9 * max(t1, t2 if tk == 2 else 0)
+        rate = 1e9 * max(t1, rates.get(tk, 0.0))
         step_s = nx * ny * nzl / rate
         best = None
         for cand in (1, 2, 4, 8, 16):
