@@ -153,16 +153,16 @@ constexpr KernelEntry make_entry1() {
 template <int R, bool WAVE, int NCW, int VY>
 cudaError_t launch_sweep1s(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                            size_t smem, cudaStream_t stream) {
-  const int block = 32 * (NCW + 1);
+  const int block = Geom1S<R, NCW, VY, WAVE>::NTHREADS;
   if (p.outS)
-    return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 1>, grid, block, smem, stream, maps.u, p, nslot);
+    return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 1>, grid, block, smem, stream, maps, p, nslot);
   if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi)
-    return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 2>, grid, block, smem, stream, maps.u, p, nslot);
+    return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 2>, grid, block, smem, stream, maps, p, nslot);
   if constexpr (R >= 7) {
     if (p.iso)
-      return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0, true>, grid, block, smem, stream, maps.u, p, nslot);
+      return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0, true>, grid, block, smem, stream, maps, p, nslot);
   }
-  return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0>, grid, block, smem, stream, maps.u, p, nslot);
+  return launch_pdl(sweep1s_kernel<R, WAVE, NCW, VY, 0>, grid, block, smem, stream, maps, p, nslot);
 }
 
 template <int R, bool WAVE, int NCW, int VY>
@@ -191,10 +191,11 @@ template <int R, bool WAVE, int NCW, int VY>
 constexpr KernelEntry make_entry1s() {
   using G = Geom1<R, 3, NCW, VY>;
   using S = Geom1S<R, NCW, VY, WAVE>;
-  KernelEntry e{3, WAVE ? 2 : 1, R, 1, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+  KernelEntry e{3, WAVE ? 2 : 1, R, 1, VY, NCW, S::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                 R, (size_t)S::SLOT_BYTES, (size_t)S::FIXED_BYTES,
                 &launch_sweep1s<R, WAVE, NCW, VY>, &query_sweep1s<R, WAVE, NCW, VY>, S::NS - R - 1};
   e.fixed_slots = S::NS;
+  if (S::TMAE) { e.ebw = 64; e.eh0 = S::OY; e.eh1 = S::OY; }   // host encodes the u^{n-1} / medium maps
   return e;
 }
 

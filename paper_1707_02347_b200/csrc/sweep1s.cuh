@@ -17,8 +17,14 @@
 // cp.async staging fit in shared memory and it measured faster); other shapes keep sweep1_kernel.
 #pragma once
 #include "sweep1.cuh"
+#include "sweep2.cuh"   // 32-bit shared-window TMA helper
 
 namespace st {
+
+#ifndef ST_S1S_TMAE
+#define ST_S1S_TMAE 1   // 1: u^{n-1} and the medium arrive by TMA (second producer warp, E ring);
+                        // 0: per-warp cp.async staging (round-1 design, for A/B builds)
+#endif
 
 template <int R, int NCW, int VY, bool WAVE>
 struct Geom1S {
@@ -29,20 +35,32 @@ struct Geom1S {
   static constexpr int STAGE_F = B::STAGE_F;
   static constexpr int SMEM_MAX = 227 * 1024;
   static constexpr int BAR_BYTES = 1024;
+  static constexpr bool TMAE = WAVE && ST_S1S_TMAE;
+  // TMA E ring (TMAE): per output plane, the tile's u^{n-1} box (64 x OY) then its medium box
+  // ({a,a,c,c} per pair: 128 floats x OY); DE entries, as many as shared memory allows (<= 8)
+  static constexpr int OY = NCW * VY;
+  static constexpr int E_FIELD = (64 * OY * 4 + 127) / 128 * 128;
+  static constexpr int E_BYTES = E_FIELD + 128 * OY * 4;
+  static constexpr int DE_FIT = (SMEM_MAX - BAR_BYTES - NS * SLOT_BYTES) / E_BYTES;
+  static constexpr int DE = DE_FIT > 8 ? 8 : DE_FIT;
   static constexpr int stage_bytes(int pd) { return NCW * (pd + 1) * STAGE_F * 4; }
   static constexpr bool fits(int pd) {
-    return BAR_BYTES + NS * SLOT_BYTES + (WAVE ? stage_bytes(pd) : 0) <= SMEM_MAX;
+    return BAR_BYTES + NS * SLOT_BYTES + (WAVE && !TMAE ? stage_bytes(pd) : 0) <= SMEM_MAX;
   }
   static constexpr int PD = fits(4) ? 4 : 3;                 // cp.async staging distance (planes)
-  static constexpr bool OK = fits(PD);
-  static constexpr int FIXED_BYTES = BAR_BYTES + (WAVE ? stage_bytes(PD) : 0);
+  static constexpr bool OK = TMAE ? DE >= 2 : fits(PD);
+  static constexpr int FIXED_BYTES = BAR_BYTES + (TMAE ? DE * E_BYTES : WAVE ? stage_bytes(PD) : 0);
+  static constexpr int NPROD = TMAE ? 2 : 1;                 // producer warps
+  static constexpr int NTHREADS = 32 * (NCW + NPROD);
+  static_assert(!TMAE || (FIXED_BYTES % 128 == 0), "TMA ring alignment");
 };
 
 // MODE: 0 plain, 1 snapshot store (SAVE), 2 fused halo push (PUSH), as sweep1_kernel.
 template <int R, bool WAVE, int NCW, int VY, int MODE, bool ISO = false>
-__global__ void __launch_bounds__(32 * (NCW + 1), 1)
-sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
+__global__ void __launch_bounds__(Geom1S<R, NCW, VY, WAVE>::NTHREADS, 1)
+sweep1s_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ SweepParams p,
                const int nslot_unused) {
+  const CUtensorMap& tmapC = maps.u;
   constexpr bool SAVE = MODE == 1, PUSH = MODE == 2;
   using G = Geom1<R, 3, NCW, VY>;
   using S = Geom1S<R, NCW, VY, WAVE>;
@@ -50,10 +68,14 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
   constexpr int QN = S::QN, NS = S::NS, BW = G::BW, RXB = G::RXB;
   constexpr int SLOT_F = S::SLOT_BYTES / 4;
   constexpr int PD = S::PD, STAGE_F = S::STAGE_F;
+  constexpr bool TMAE = S::TMAE;
+  constexpr int DE = S::DE, EB = S::E_BYTES;
 
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NS;
+  uint64_t* efull = full + 2 * NS;                // E ring (TMAE)
+  uint64_t* eempty = efull + 8;
   float* stage0 = reinterpret_cast<float*>(smem + S::BAR_BYTES);
   float* ring = reinterpret_cast<float*>(smem + S::FIXED_BYTES);
 
@@ -71,11 +93,32 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 32 * NCW);
     }
+    if (TMAE)
+      for (int i = 0; i < DE; ++i) {
+        mbar_init(&efull[i], 1);
+        mbar_init(&eempty[i], 32 * NCW);
+      }
     fence_mbar_init();
   }
   __syncthreads();
   pdl_prologue_done();
 
+  if (TMAE && warp == NCW + 1) {
+    // ------------------------------------------------- producer warp 2: u^{n-1} + medium per plane
+    if (lane == 0) {
+      int es = 0;
+      uint32_t eph = 0;
+      const uint32_t ebase = smem_u32(smem + S::BAR_BYTES);
+      for (int s = zb; s < ze; ++s) {
+        if (s - zb >= DE) mbar_wait(&eempty[es], eph ^ 1u);
+        mbar_expect_tx(&efull[es], (uint32_t)(192 * S::OY * 4));   // both boxes, OOB zero-filled
+        tma_load_3d_s(ebase + es * EB, &maps.p0, smem_u32(&efull[es]), tx0, ty0, s - p.zv_lo);
+        tma_load_3d_s(ebase + es * EB + S::E_FIELD, &maps.a0, smem_u32(&efull[es]), 2 * tx0, ty0, s - p.zv_lo);
+        if (++es == DE) { es = 0; eph ^= 1u; }
+      }
+    }
+    return;
+  }
   if (warp == NCW) {
     // ------------------------------------------------------------------ producer warp
     if (lane == 0) {
@@ -152,10 +195,16 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
     e_iss += STAGE_F;
     if (e_iss == stage_end) e_iss = stage;
   };
-  if (WAVE) {
+  if (WAVE && !TMAE) {
 #pragma unroll 1
     for (int i = 0; i < PD; ++i) stage_next();
   }
+  // E ring (TMAE): my u^{n-1} pair and medium float4 of row j inside an entry
+  const float* e_slot = reinterpret_cast<const float*>(smem + S::BAR_BYTES);
+  const int e_pv = (warp * VY) * 64 + 2 * lane;
+  const int e_ac = S::E_FIELD / 4 + (warp * VY) * 128 + 4 * lane;
+  int es = 0;
+  uint32_t eph = 0;
 
   uint64_t qn[QN][VY];
 #pragma unroll
@@ -165,7 +214,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
 
   // one output plane: centre = queue entry / ring slot CS (compile-time after unrolling)
   auto compute = [&](const int CS, const int s) {
-    if (WAVE) stage_next();                       // plane s + PD
+    if (WAVE && !TMAE) stage_next();              // plane s + PD
     uint64_t acc[VY];
     accumulate<R, R, QN, VY, 3, BW, ISO>(acc, qn, rcol + CS * SLOT_F, p, CS);
     if (wsrc) {
@@ -174,7 +223,21 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
         if (yin[j]) acc[j] = add_sources_row(acc[j], p, s, y0 + j, x0, p.wl_step);
     }
     uint64_t o[VY];
-    if (WAVE) {
+    if (TMAE) {
+      mbar_wait(&efull[es], eph);
+      const float* e = e_slot + es * (EB / 4);
+      uint32_t z = 0;
+#pragma unroll
+      for (int j = 0; j < VY; ++j) {
+        const uint64_t c = qn[CS][j];
+        const uint64_t pv = lds64(e + e_pv + j * 64);
+        const float4 m4 = *reinterpret_cast<const float4*>(e + e_ac + j * 128);
+        z |= zero_after(pv, p.zero) | zero_after(pack2(m4.x, m4.w), p.zero);
+        o[j] = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c)) & mask[j];
+      }
+      mbar_arrive(&eempty[es] + z);      // release the entry once my loads from it have returned
+      if (++es == DE) { es = 0; eph ^= 1u; }
+    } else if (WAVE) {
       cp_async_wait<PD>();
 #pragma unroll
       for (int j = 0; j < VY; ++j) {
@@ -252,7 +315,7 @@ sweep1s_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant_
     }
     ph ^= 1u;
   }
-  if (WAVE) cp_async_wait<0>();
+  if (WAVE && !TMAE) cp_async_wait<0>();
   if (PUSH) signal_peers(p, push_lo, push_hi, 32 * NCW);
 }
 
