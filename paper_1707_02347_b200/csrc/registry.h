@@ -99,20 +99,20 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, int block, size_t sm
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
 cudaError_t launch_sweep1(const KernelMaps& maps, const SweepParams& p, dim3 grid, int nslot,
                           size_t smem, cudaStream_t stream) {
-  const int block = 32 * (NCW + 1);
+  const int block = Geom1E<R, NDIM, NCW, VY, WAVE>::NTHREADS;
   if (p.outS)
-    return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 1>, grid, block, smem, stream, maps.u, p, nslot);
+    return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 1>, grid, block, smem, stream, maps, p, nslot);
   if (p.push_lo || p.push_hi || p.wait_lo || p.wait_hi) {
     if constexpr (NDIM == 3)
-      return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 2>, grid, block, smem, stream, maps.u, p, nslot);
+      return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 2>, grid, block, smem, stream, maps, p, nslot);
     else
       return cudaErrorNotSupported;
   }
   if constexpr (NDIM == 3 && R >= 7) {   // measured: C4 SO16 239 -> 245 GPts/s; SO12 unchanged
     if (p.iso)
-      return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0, true>, grid, block, smem, stream, maps.u, p, nslot);
+      return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0, true>, grid, block, smem, stream, maps, p, nslot);
   }
-  return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0>, grid, block, smem, stream, maps.u, p, nslot);
+  return launch_pdl(sweep1_kernel<R, WAVE, NDIM, NCW, VY, 0>, grid, block, smem, stream, maps, p, nslot);
 }
 
 template <int R, bool WAVE, int NDIM, int NCW, int VY>
@@ -144,9 +144,12 @@ cudaError_t query_sweep1(size_t smem, cudaFuncAttributes* attr, int* bps, int nt
 template <int R, bool WAVE, int NDIM, int NCW, int VY = 1>
 constexpr KernelEntry make_entry1() {
   using G = Geom1<R, NDIM, NCW, VY>;
-  return KernelEntry{NDIM, WAVE ? 2 : 1, R, 1, VY, NCW, G::NTHREADS, G::OX, G::OY, G::BW, G::BH,
-                     G::RZ, (size_t)G::SLOT_BYTES, (size_t)1024 + (WAVE ? G::STAGE_BYTES : 0),
-                     &launch_sweep1<R, WAVE, NDIM, NCW, VY>, &query_sweep1<R, WAVE, NDIM, NCW, VY>, ST_T1_DEPTH};
+  using GE = Geom1E<R, NDIM, NCW, VY, WAVE>;
+  KernelEntry e{NDIM, WAVE ? 2 : 1, R, 1, VY, NCW, GE::NTHREADS, G::OX, G::OY, G::BW, G::BH,
+                G::RZ, (size_t)G::SLOT_BYTES, (size_t)GE::FIXED_BYTES,
+                &launch_sweep1<R, WAVE, NDIM, NCW, VY>, &query_sweep1<R, WAVE, NDIM, NCW, VY>, ST_T1_DEPTH};
+  if (GE::TMAE) { e.ebw = 64; e.eh0 = GE::OY; e.eh1 = GE::OY; }   // host encodes the u^{n-1} / medium maps
+  return e;
 }
 
 // ---- untiled kernel with a compiled-in ring of 2r+1 slots (sweep1s.cuh)

@@ -33,6 +33,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
+__device__ __forceinline__ void tma_load_3d_e(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                              int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
 // Rare paths kept out of the unrolled body (called only by warps whose row holds an event).
 static __device__ __noinline__ uint64_t add_sources_row(uint64_t acc, const SweepParams& p, int s, int y,
                                                  int x0, long long wl_step) {
@@ -81,6 +90,27 @@ struct Geom1 {
   static_assert(BW <= 256 && BH <= 256, "TMA box limit");
 };
 
+#ifndef ST_S1_TMAE
+#define ST_S1_TMAE 1    // 3-D wave: u^{n-1} and the medium arrive by TMA (E ring, second producer warp)
+#endif
+// E ring of the untiled 3-D wave kernels: per output plane, the tile's u^{n-1} box (64 x OY) and
+// its medium box ({a,a,c,c} per pair: 128 floats x OY), DE entries.  TMA writes into shared memory
+// do not use the 128 B/clk/SM LDS crossbar that cp.async staging fills twice.
+template <int R, int NDIM, int NCW, int VY, bool WAVE>
+struct Geom1E {
+  // measured (same box): C3 SO8 332.8 vs 320.6 GPts/s with the E ring; wave SO2 323.6 vs 334.2
+  static constexpr bool TMAE = WAVE && NDIM == 3 && R >= 3 && ST_S1_TMAE;
+  static constexpr int OY = NCW * VY;
+  static constexpr int E_FIELD = (64 * OY * 4 + 127) / 128 * 128;
+  static constexpr int E_BYTES = E_FIELD + 128 * OY * 4;
+  static constexpr int DE = 4;
+  static constexpr int NPROD = TMAE ? 2 : 1;
+  static constexpr int NTHREADS = 32 * (NCW + NPROD);
+  static constexpr int BAR_BYTES = 1024;   // full/empty of <= 56 ring slots, E full/empty
+  static constexpr int FIXED_BYTES = BAR_BYTES + (TMAE ? DE * E_BYTES
+                                                       : WAVE ? Geom1<R, NDIM, NCW, VY>::STAGE_BYTES : 0);
+};
+
 // Is any table entry (sorted by plane) on planes [z0, z1) in row y, columns [x0, x1)?
 __device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent, int z0, int z1,
                                               int y, int x0, int x1) {
@@ -98,9 +128,13 @@ __device__ __forceinline__ bool row_has_entry(const int* begin, const int4* ent,
 // snapshot or push logic in its step body (measured: the push checks cost C4 11 %).
 // ISO: isotropic-weight instance (see accumulate), launched when p.iso (3-D, r >= 7, MODE 0).
 template <int R, bool WAVE, int NDIM, int NCW, int VY, int MODE, bool ISO = false>
-__global__ void __launch_bounds__(32 * (NCW + 1), 1)
-sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__ SweepParams p,
+__global__ void __launch_bounds__(Geom1E<R, NDIM, NCW, VY, WAVE>::NTHREADS, 1)
+sweep1_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ SweepParams p,
               const int nslot) {
+  const CUtensorMap& tmapC = maps.u;
+  using GE = Geom1E<R, NDIM, NCW, VY, WAVE>;
+  constexpr bool TMAE = GE::TMAE;
+  constexpr int DE = GE::DE, EB = GE::E_BYTES;
   constexpr bool SAVE = MODE == 1, PUSH = MODE == 2;
   using G = Geom1<R, NDIM, NCW, VY>;
   constexpr int RZ = G::RZ, QN = G::QN, RX2 = G::RX2, RXB = G::RXB, BW = G::BW;
@@ -110,7 +144,9 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + nslot;
-  float* ring = reinterpret_cast<float*>(smem + ((16 * nslot + 127) / 128) * 128);
+  uint64_t* efull = full + 112;                  // E ring barriers (TMAE), bytes 896..1023
+  uint64_t* eempty = efull + 8;
+  float* ring = reinterpret_cast<float*>(smem + GE::FIXED_BYTES);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -126,11 +162,33 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 32 * NCW);   // every consumer lane arrives
     }
+    if (TMAE)
+      for (int i = 0; i < DE; ++i) {
+        mbar_init(&efull[i], 1);
+        mbar_init(&eempty[i], 32 * NCW);
+      }
     fence_mbar_init();
   }
   __syncthreads();
   pdl_prologue_done();
 
+  if (TMAE && warp == NCW + 1) {
+    // ------------------------------------------------- producer warp 2: u^{n-1} + medium per plane
+    if (lane == 0) {
+      int es = 0;
+      uint32_t eph = 0;
+      const uint32_t ebase = static_cast<uint32_t>(__cvta_generic_to_shared(smem + GE::BAR_BYTES));
+      for (int s = zb; s < ze; ++s) {
+        if (s - zb >= DE) mbar_wait(&eempty[es], eph ^ 1u);
+        mbar_expect_tx(&efull[es], (uint32_t)(192 * GE::OY * 4));   // both boxes, OOB zero-filled
+        const uint32_t fb = static_cast<uint32_t>(__cvta_generic_to_shared(&efull[es]));
+        tma_load_3d_e(ebase + es * EB, &maps.p0, fb, tx0, ty0, s - p.zv_lo);
+        tma_load_3d_e(ebase + es * EB + GE::E_FIELD, &maps.a0, fb, 2 * tx0, ty0, s - p.zv_lo);
+        if (++es == DE) { es = 0; eph ^= 1u; }
+      }
+    }
+    return;
+  }
   if (warp == NCW) {
     // ------------------------------------------------------------------ producer warp
     if (lane == 0) {
@@ -189,7 +247,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   // Every plane of [zb, ze) lies inside the global domain (host invariant), so each step computes.
   const long long plane = p.plane;
   const int X = p.X, X2 = p.X >> 1;
-  float* stage = ring + (size_t)nslot * SLOT_F + (size_t)warp * (PD + 1) * STAGE_F;
+  float* stage = reinterpret_cast<float*>(smem + GE::BAR_BYTES) + (size_t)warp * (PD + 1) * STAGE_F;
   const int s0 = zb - 2 * RZ;                       // level-0 plane of arrival 0
   const float* gP = p.P + (long long)zb * plane + (long long)y0 * X + x0;   // plane zb
   const float4* gA = p.ac + (long long)zb * (plane >> 1) + (long long)y0 * X2 + (x0 >> 1);
@@ -212,10 +270,15 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     gP += plane; gA += plane >> 1; ++q_iss;
     if (++e_iss == PD + 1) e_iss = 0;
   };
-  if (WAVE) {
+  if (WAVE && !TMAE) {
 #pragma unroll 1
     for (int i = 0; i < PD; ++i) stage_next();
   }
+  const float* e_slot = reinterpret_cast<const float*>(smem + GE::BAR_BYTES);
+  const int e_pv = (warp * VY) * 64 + 2 * lane;
+  const int e_ac = GE::E_FIELD / 4 + (warp * VY) * 128 + 4 * lane;
+  int es = 0;
+  uint32_t eph = 0;
 
   uint64_t qn[QN][VY];
 #pragma unroll
@@ -248,7 +311,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
           mbar_arrive(&empty[slot_a] + z);
         }
         if (idx >= 2 * RZ) {                          // step s = s0 + idx in [zb, ze)
-          if (WAVE) stage_next();                     // plane s + PD
+          if (WAVE && !TMAE) stage_next();            // plane s + PD
           const int s = s0 + idx;
           const float* rp = ring + slot_s * SLOT_F + col;
           uint64_t acc[VY];
@@ -259,7 +322,21 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
               if (yin[j]) acc[j] = add_sources_row(acc[j], p, s, y0 + j, x0, p.wl_step);
           }
           uint64_t o[VY];
-          if (WAVE) {
+          if (TMAE) {
+            mbar_wait(&efull[es], eph);
+            const float* e = e_slot + es * (EB / 4);
+            uint32_t z = 0;
+#pragma unroll
+            for (int j = 0; j < VY; ++j) {
+              const uint64_t c = qn[md<QN>(u - RZ)][j];
+              const uint64_t pv = lds64(e + e_pv + j * 64);
+              const float4 m4 = *reinterpret_cast<const float4*>(e + e_ac + j * 128);
+              z |= zero_after(pv, p.zero) | zero_after(pack2(m4.x, m4.w), p.zero);
+              o[j] = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c)) & mask[j];
+            }
+            mbar_arrive(&eempty[es] + z);    // release the entry once my loads from it have returned
+            if (++es == DE) { es = 0; eph ^= 1u; }
+          } else if (WAVE) {
             cp_async_wait<PD>();                      // the group of plane s has landed
             const float* st_e = stage + e_use * STAGE_F;
 #pragma unroll
@@ -314,7 +391,7 @@ sweep1_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       }
     }
   }
-  if (WAVE) cp_async_wait<0>();
+  if (WAVE && !TMAE) cp_async_wait<0>();
   if (PUSH) signal_peers(p, push_lo, push_hi, 32 * NCW);
 }
 
