@@ -127,13 +127,11 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   const uint64_t xmask = (xin0 ? 0xffffffffull : 0ull) | (xin1 ? 0xffffffff00000000ull : 0ull);
   const int wr = warp * VY;                          // my first region row
   const int y0 = gy + wr;
-  uint64_t mask[VY];
   unsigned smask = 0;                                // bit j: row j is an output row in the domain
   unsigned ymask = 0;                                // bit j: row j is in the domain
 #pragma unroll
   for (int j = 0; j < VY; ++j) {
     const bool yin = (y0 + j >= 0) && (y0 + j < p.ny);
-    mask[j] = yin ? xmask : 0ull;
     ymask |= yin ? (1u << j) : 0u;
     smask |= (yin && (wr + j >= HY) && (wr + j < GH - HY)) ? (1u << j) : 0u;
   }
@@ -167,10 +165,13 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   const uint64_t DT = splat(p.dt), K0 = splat(p.K0);
   const long long plane = p.plane;
   const int X = p.X;
-  float* const oc = p.outC + (long long)y0 * X + x0;   // my first row / pair, plane 0
-  float* const op = p.outP + (long long)y0 * X + x0;
-  float* const os = SAVE ? p.outS + (long long)y0 * X + x0 : nullptr;
+  // output pointer of the last level's plane at step a (advances by one plane per step);
+  // u^{n+TK-1} and the snapshot live at fixed element distances from it
+  float* oz = p.outC + (long long)(p_first - TK * R) * plane + (long long)y0 * X + x0;
+  const long long dP = p.outP - p.outC, dS = SAVE ? p.outS - p.outC : 0;
   const bool wprev = p.write_prev != 0;
+  // the region lies inside the domain: no level output needs the Dirichlet mask (CTA-uniform)
+  const bool edge = !(gx >= 0 && gx + GW <= p.nx && gy >= 0 && gy + GH <= p.ny);
 
   // steady steps: every level's queue is full and its plane inside the global interior
   int st_lo = 2 * TK * R, st_hi = n_arr;
@@ -193,8 +194,9 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
   int bw_ = 0;                            // boundary slot written at step a (a mod D)
 
   // one step (arrival a, queue index UU = a mod QN); CHECK: prologue / epilogue / boundary steps
-  auto step = [&](auto CHK, auto UU, const int a) {
+  auto step = [&](auto CHK, auto EDG, auto UU, const int a) {
     constexpr bool CHECK = decltype(CHK)::value;
+    constexpr bool EDGE = decltype(EDG)::value;
     constexpr int iN = decltype(UU)::value, iC = md<QN>(iN - R);
     if (CHECK && a >= n_arr) return;
     const int br = (bw_ + 1 == D) ? 0 : bw_ + 1;   // (a - R) mod D
@@ -251,7 +253,10 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
             if ((ymask >> j) & 1) acc[j] = add_sources_row(acc[j], p, z, y0 + j, x0, p.wl_step + l);
         }
 #pragma unroll
-        for (int j = 0; j < VY; ++j) o[j] = f2fma(DT, acc[j], q[l][iC][j]) & mask[j];
+        for (int j = 0; j < VY; ++j) {
+          o[j] = f2fma(DT, acc[j], q[l][iC][j]);
+          if (EDGE) o[j] &= ((ymask >> j) & 1) ? xmask : 0ull;
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < VY; ++j) o[j] = 0ull;
@@ -269,18 +274,18 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       } else {
         // u^{n+TK} (and u^{n+TK-1} on the last pass) on the output tile
         if (act && smask) {
-          const long long zo = (long long)z * plane;
 #pragma unroll
           for (int j = 0; j < VY; ++j) {
             if ((smask >> j) & 1) {
+              float* d = oz + j * X;
               if (xin1) {
-                sts64(oc + zo + j * X, o[j]);
-                if (wprev) sts64(op + zo + j * X, q[l][iC][j]);
-                if (SAVE) sts64(os + zo + j * X, o[j]);
+                sts64(d, o[j]);
+                if (wprev) sts64(d + dP, q[l][iC][j]);
+                if (SAVE) sts64(d + dS, o[j]);
               } else {
-                oc[zo + j * X] = lo_of(o[j]);
-                if (wprev) op[zo + j * X] = lo_of(q[l][iC][j]);
-                if (SAVE) os[zo + j * X] = lo_of(o[j]);
+                d[0] = lo_of(o[j]);
+                if (wprev) d[dP] = lo_of(q[l][iC][j]);
+                if (SAVE) d[dS] = lo_of(o[j]);
               }
             }
           }
@@ -304,16 +309,21 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     }
     if (++s_a == nslot) { s_a = 0; ph_a ^= 1u; }
     if (++bw_ == D) bw_ = 0;
+    oz += plane;
   };
 
+  auto run = [&](auto EDG) {
 #pragma unroll 1
-  for (int base = 0; base < n_arr; base += QN) {
-    if (base >= st_lo && base + QN <= st_hi) {
-      static_for<0, QN>([&](auto UU) { step(std::false_type{}, UU, base + decltype(UU)::value); });
-    } else {
-      static_for<0, QN>([&](auto UU) { step(std::true_type{}, UU, base + decltype(UU)::value); });
+    for (int base = 0; base < n_arr; base += QN) {
+      if (base >= st_lo && base + QN <= st_hi) {
+        static_for<0, QN>([&](auto UU) { step(std::false_type{}, EDG, UU, base + decltype(UU)::value); });
+      } else {
+        static_for<0, QN>([&](auto UU) { step(std::true_type{}, EDG, UU, base + decltype(UU)::value); });
+      }
     }
-  }
+  };
+  if (edge) run(std::true_type{});
+  else run(std::false_type{});
 }
 
 }  // namespace st
