@@ -287,7 +287,7 @@ def _kernel_name(p: W.Problem, tk: int) -> str:
         return f"st::resident2d_kernel<R={p.radius}, wave={int(p.time_order == 2)}> (whole run)"
     from paper_1707_02347_b200.build import instances
     names = {0: "st::sweep_kernel", 1: "st::sweep1_kernel", 2: "st::sweep2_kernel", 3: "st::sweep1s_kernel",
-             4: "st::sweepx_kernel"}
+             4: "st::sweepx_kernel", 5: "st::sweeph_kernel"}
     for (ndim, wave, R, TK, VY, NWY, kind) in instances():
         if (ndim, wave, R, TK) == (p.ndim, int(p.time_order == 2), p.radius, tk):
             return f"{names.get(kind, f'kind{kind}')}<R={R}, T_k={TK}>"
