@@ -80,7 +80,10 @@ def _exch(wave: int, R: int) -> bool:
     return bool(wave) and R >= 3
 
 
-HEAT_H = (4, 16)   # (rows per warp, warps) of the register-resident heat time-tiled kernel (kind 5)
+# T_k -> (rows per warp, warps) of sweeph (kind 5): regions of 68 / 70 / 72 rows keep a 64-row output
+# tile (256 and 512 split into whole tiles); measured same box vs 64-row regions (4 x 16), GPts/s:
+# C2 T_k=2/3/4 904/980/1017 vs 780/873/878; 512^3 1176/1169/1205 vs 1186/1224/1094
+HEAT_H = {2: (4, 17), 3: (5, 14), 4: (6, 12)}
 
 
 def _heat_h(R: int, TK: int) -> bool:
@@ -99,7 +102,7 @@ def instances():
             out.append((3, wave, R, 1, vy, ncw, 3 if _static_ring(3, wave, R) else 1))
             oy = _sweep2_oy(wave, R, 2)
             if not wave and _heat_h(R, 2):
-                out.append((3, 0, R, 2) + HEAT_H + (5,))
+                out.append((3, 0, R, 2) + HEAT_H[2] + (5,))
             elif _exch(wave, R):
                 out.append((3, wave, R, 2, vy, ncw, 4))        # L1/L2 roles, untiled geometry
             elif oy:
@@ -113,10 +116,10 @@ def instances():
         out.append((2, wave, 1, 4) + _vy_nwy(2, 1, 4) + (0,))
     # heat T_k = 4 (sweep2); T_k = 8 (first-generation kernel, 46 GPts/s on 512^3 vs 708 at T = 1)
     # is retired: stencil_create reports ST_EUNSUPPORTED for it
-    out.append((3, 0, 1, 3) + HEAT_H + (5,))
+    out.append((3, 0, 1, 3) + HEAT_H[3] + (5,))
     for R, TK in ((1, 4), (2, 4)):
         if _heat_h(R, TK):
-            out.append((3, 0, R, TK) + HEAT_H + (5,))
+            out.append((3, 0, R, TK) + HEAT_H[TK] + (5,))
             continue
         oy = _sweep2_oy(0, R, TK)
         out.append((3, 0, R, TK, 2, oy, 2) if oy else (3, 0, R, TK) + _vy_nwy(3, R, TK) + (0,))
@@ -226,7 +229,7 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
 
 
 def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = True,
-                  static_r=None, oy2=None) -> str:
+                  static_r=None, oy2=None, heat_h=None) -> str:
     """Experimental library _variants/libstencil_<name>.so with extra -D flags and (optionally)
     only the instances whose (ndim, wave, R, TK) is listed; load it with ST_LIB=<path>."""
     inst = instances()
@@ -240,6 +243,8 @@ def build_variant(name: str, defines=(), only=None, t1=None, verbose: bool = Tru
     if static_r is not None:   # radii whose 3-D untiled instances use the static ring (kind 3)
         inst = [i[:6] + ((3 if i[2] in static_r else 1),) if i[0] == 3 and i[3] == 1 and i[6] in (1, 3)
                 else i for i in inst]
+    if heat_h is not None:   # {T_k: (rows per warp, warps)} of the heat time-tiled kernel (kind 5)
+        inst = [i[:4] + heat_h.get(i[3], (i[4], i[5])) + i[6:] if i[6] == 5 else i for i in inst]
     if t1 is not None:   # (consumer warps, rows per warp) of the untiled kernel
         inst = [i[:4] + (t1[1], t1[0], i[6]) if i[6] in (1, 3) else i for i in inst]
     return _build(outdir, lib, inst, list(defines), groups=4, verbose=verbose)

@@ -78,11 +78,11 @@ _MEASURED = {  # (time_order, radius): {T_k: GPts/s}
     (2, 1): {1: 334.5, 2: 424.8}, (2, 2): {1: 332.7, 2: 380.0}, (2, 3): {1: 321.7, 2: 264.1},
     (2, 4): {1: 319.6, 2: 250.4}, (2, 5): {1: 326.2, 2: 228.8}, (2, 6): {1: 318.7, 2: 205.9},
     (2, 7): {1: 264.8, 2: 178.4}, (2, 8): {1: 247.5, 2: 118.2},
-    (1, 1): {1: 729.9, 2: 1187.9, 3: 1234.5, 4: 1090.7},
+    (1, 1): {1: 735.8, 2: 1176.3, 3: 1169.2, 4: 1204.7},
 }
 # grids whose own measurement differs from the 512^3 ranking (tile raggedness, L2 residency)
 _MEASURED_GRID = {
-    (1, 1, (256, 256, 256)): {1: 625.0, 2: 776.5, 3: 874.2, 4: 873.2},   # C2
+    (1, 1, (256, 256, 256)): {1: 625.3, 2: 904.2, 3: 980.4, 4: 1017.4},   # C2
 }
 NVLINK_GBS = 770.0          # measured peer copy per direction (B200_PROFILING.md)
 EXCHANGE_LATENCY_US = 25.0  # NCCL send/recv launch + sync per exchange (estimate)
