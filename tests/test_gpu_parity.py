@@ -266,8 +266,9 @@ def test_t1_band_interior_split(monkeypatch, order):
 
 
 # ----------------------------------------------------------------------------- library-owned exchange
-@pytest.mark.parametrize("t_comm,t_kernel", [(1, 1), (3, 1), (4, 2)])
-def test_lib_exchange_single_rank(t_comm, t_kernel):
+@pytest.mark.parametrize("t_comm,t_kernel,heat", [(1, 1, False), (3, 1, False), (4, 2, False),
+                                                  (8, 4, True), (6, 3, True)])
+def test_lib_exchange_single_rank(t_comm, t_kernel, heat):
     """st_config.nccl_id on a one-rank plan: the library-owned time loop (T_c periods, NCCL group
     calls with no neighbours, comm-stream joins, trace zeroing and ncclAllReduce) runs for real on
     one GPU and stays bit-exact; the multi-rank transfers need >= 2 GPUs."""
@@ -275,14 +276,17 @@ def test_lib_exchange_single_rank(t_comm, t_kernel):
     from paper_1707_02347_b200 import Stencil
     from paper_1707_02347_b200.stencil import nccl_unique_id
     p = _wave("C3", (60, 44, 36), 11, 5, src=[(30, 22, 18)], rec=[(30, 22, 18), (5, 40, 2), (59, 0, 35)])
+    if heat:   # the heat time-tiled kernel (sweeph) inside the library's period loop
+        p = W.Problem(**{**W.problem("C2", n=(60, 44, 36), nt=19).__dict__, "f_peak": 15.0,
+                         "src": p.src, "rec": p.rec})
     st = Stencil(p.ndim, p.n, p.space_order, p.time_order, p.dt, p.dx, t_kernel=t_kernel,
                  t_comm=t_comm, nccl_id=nccl_unique_id())
     assert st.lib_exchange
     up, uc = W.initial_fields(p)
     P = st.embed(torch.from_numpy(up).cuda())
     C = st.embed(torch.from_numpy(uc).cuda())
-    vel = st.embed(torch.from_numpy(W.velocity(p)).cuda())
-    damp = st.embed(torch.from_numpy(W.damp(p)).cuda())
+    vel = st.embed(torch.from_numpy(W.velocity(p)).cuda()) if not heat else None
+    damp = st.embed(torch.from_numpy(W.damp(p)).cuda()) if not heat else None
     wav = torch.from_numpy(W.wavelet(p, p.nt)).cuda()
     trace = torch.full((p.nt, len(p.rec)), float("nan"), device="cuda")   # the library zeroes it
     st.run(P, C, p.nt, vel=vel, damp=damp, src=list(p.src), wavelet=wav, rec=list(p.rec), trace=trace)
