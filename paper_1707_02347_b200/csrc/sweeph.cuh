@@ -28,6 +28,10 @@
 
 namespace st {
 
+#ifndef ST_H_STEADY
+#define ST_H_STEADY 1
+#endif
+
 template <int R, int TK, int VY, int NW>
 struct GeomH {
   static constexpr int GW = 64;
@@ -312,10 +316,13 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
     oz += plane;
   };
 
+  // ST_H_STEADY: compile a check-free step body for the steady blocks (1) or run every block with
+  // the uniform level/plane checks (0: half the code; the kernel is instruction-cache bound at
+  // T_k = 4 with 6-row strips, ncu no_instruction stalls)
   auto run = [&](auto EDG) {
 #pragma unroll 1
     for (int base = 0; base < n_arr; base += QN) {
-      if (base >= st_lo && base + QN <= st_hi) {
+      if (ST_H_STEADY && base >= st_lo && base + QN <= st_hi) {
         static_for<0, QN>([&](auto UU) { step(std::false_type{}, EDG, UU, base + decltype(UU)::value); });
       } else {
         static_for<0, QN>([&](auto UU) { step(std::true_type{}, EDG, UU, base + decltype(UU)::value); });
