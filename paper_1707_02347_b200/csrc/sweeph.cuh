@@ -329,7 +329,10 @@ sweeph_kernel(const __grid_constant__ CUtensorMap tmapC, const __grid_constant__
       }
     }
   };
-  if (edge) run(std::true_type{});
+#ifndef ST_H_EDGE_SPLIT
+#define ST_H_EDGE_SPLIT 1   // 0: one body that always applies the Dirichlet mask (half the code)
+#endif
+  if (edge || !ST_H_EDGE_SPLIT) run(std::true_type{});
   else run(std::false_type{});
 }
 
