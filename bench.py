@@ -163,17 +163,17 @@ def run_gpu(args):
         runner.reset_state(dev_in)          # zero initial fields (device memset, part of the step)
         return runner.run(dev_in, nt)
 
-    # warm-up
+    # clock sampler first (its start waits for the first nvidia-smi sample, an idle gap that would
+    # let the SM clock drop), then the warm-up steps right before the timed region
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step_resident()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    runner.set_timing(True)     # per-run sweep events on the plan's stream, no host sync
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -182,12 +182,21 @@ def run_gpu(args):
         step_resident()
     e1.record(stream)
     torch.cuda.synchronize()
+    t_ms = e0.elapsed_time(e1)
+    # the same K steps again with the library's per-run sweep events on the plan's stream (no host
+    # sync): the roofline's per-launch kernel time.  A separate pass because timed events serialise
+    # the stream and would inflate the step time of launch-bound runs (C1: +7 us per 18 us step).
+    runner.set_timing(True)
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        step_resident()
+    torch.cuda.synchronize()
     sweep_ms, sweep_launches, tiled, aux = runner.timing()   # summed over the timed runs
     runner.set_timing(False)
     if world > 1:
         dist.barrier()
     ck = clocks.stop()
-    t_ms = e0.elapsed_time(e1)
     # max over ranks
     if world > 1:
         t = torch.tensor([t_ms], device=dev)

@@ -205,7 +205,8 @@ class SlabRunner:
 
     def reset_state(self, dev):
         dev["u_cur"].copy_(dev["_init_cur"])
-        dev["u_prev"].copy_(dev["_init_prev"])
+        if self.wave:           # heat reads only u^n: its u_prev is output-only (include/stencil.h)
+            dev["u_prev"].copy_(dev["_init_prev"])
 
     def upload(self, host, dev):
         for k in ("u_prev", "u_cur", "vel", "damp", "wavelet"):
