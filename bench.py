@@ -151,6 +151,12 @@ def run_gpu(args):
     else:
         tc = tk
     nt = p.nt if args.nt is None else args.nt
+    # launch-bound runs (the whole-run 2-D kernel: one launch of ~15 us per step) replay the step
+    # (state reset + stencil_run) as a CUDA graph captured on the plan's own stream
+    use_graph = (p.ndim == 2 and world == 1 and not args.no_graph)
+    plan_stream = torch.cuda.Stream(device=local) if use_graph else torch.cuda.current_stream(local)
+    if use_graph:
+        torch.cuda.set_stream(plan_stream)     # every torch op, event and replay on the plan's stream
     runner = SlabRunner(p, rank=rank, world=world, t_kernel=tk, t_comm=tc, device=local,
                         fused=args.fused_halo, lib_exchange=args.lib_exchange)
     st = runner.stencil
@@ -160,8 +166,29 @@ def run_gpu(args):
     fused = runner.enable_fused(dev_in) if args.fused_halo else False
 
     def step_resident():
-        runner.reset_state(dev_in)          # zero initial fields (device memset, part of the step)
+        runner.reset_state(dev_in)          # the initial fields (device copy, part of the step)
         return runner.run(dev_in, nt)
+
+    step_direct = step_resident
+    graph = None
+    if use_graph:
+        # warm, then capture one step on the plan's stream; if the library's launch sequence cannot
+        # be captured, fall back to direct calls
+        for _ in range(3):
+            step_resident()
+        torch.cuda.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=plan_stream):
+                step_resident()
+            torch.cuda.synchronize()
+            graph = g
+        except Exception as ex:          # noqa: BLE001 -- report and run uncaptured
+            print(f"bench.py: CUDA graph capture failed ({ex}); direct calls", file=sys.stderr)
+            torch.cuda.synchronize()
+    if graph is not None:
+        def step_resident():            # noqa: F811 -- the captured step (reset + stencil_run)
+            graph.replay()
 
     # clock sampler first (its start waits for the first nvidia-smi sample, an idle gap that would
     # let the SM clock drop), then the warm-up steps right before the timed region
@@ -190,7 +217,7 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     for _ in range(args.steps):
-        step_resident()
+        step_direct()
     torch.cuda.synchronize()
     sweep_ms, sweep_launches, tiled, aux = runner.timing()   # summed over the timed runs
     runner.set_timing(False)
@@ -251,6 +278,8 @@ def run_gpu(args):
                 "time_order": p.time_order, "t_kernel": tk, "t_comm": tc if world > 1 else None,
                 "schedule": pl.reason if args.tk == "auto" else f"t_kernel={tk} forced by --tk (planner: {pl.reason})",
                 "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                "step_launch": ("CUDA graph replay of one captured step (state reset + stencil_run)"
+                                if graph is not None else "direct API calls"),
                 "halo": (None if world == 1 else
                          "fused push: sweep stores band planes into peer ghost zones (P2P)" if fused
                          else "library-owned NCCL exchange (bands overlapped with the interior)"
@@ -454,6 +483,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=5, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="2-D runs: call the API per step instead of replaying a CUDA graph of it")
     ap.add_argument("--fused-halo", action="store_true",
                     help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")
     ap.add_argument("--lib-exchange", action="store_true",

@@ -60,9 +60,11 @@ __host__ __device__ inline int res_cluster(int R, int ny, int cap = RES_CLUSTER)
 // steps per cluster barrier: the halo H = r*spb must come from the two neighbours only
 // (H <= own rows of every CTA but the last), at most 8
 __host__ __device__ inline int res_spb(int R, int ny, int cs) {
+  // measured on C1 (128^2 heat, 16 CTAs of 8 rows; bench GPts/s): spb 2/3/4/6/8 ->
+  // 15.1/16.8/17.7/18.3/16.5 -- beyond 6 the redundant halo rows cost more than the barriers save
   if (cs == 1) return 8;
   int spb = 1;
-  while (spb < 8 && R * (spb + 1) <= res_own(ny, cs)) ++spb;
+  while (spb < 6 && R * (spb + 1) <= res_own(ny, cs)) ++spb;
   return spb;
 }
 
