@@ -296,3 +296,46 @@ def test_lib_exchange_single_rank(t_comm, t_kernel, heat):
     assert np.array_equal(st.interior(P).cpu().numpy(), op)
     assert np.array_equal(trace.cpu().numpy(), ot)
     st.close()
+
+
+# ----------------------------------------------------------------------------- CUDA graph replay (bench C1 path)
+@pytest.mark.parametrize("wave", [False, True])
+def test_cuda_graph_replay_2d(wave):
+    """bench.py replays the 2-D step (state reset + stencil_run) as a CUDA graph captured on the
+    plan's stream: the captured library launches must reproduce the oracle bit for bit on every
+    replay (heat: C1; wave: 2-D SO8 with a source, medium derived inside the step)."""
+    import torch
+    from paper_1707_02347_b200.dist import SlabRunner
+    if wave:
+        p = W.problem("C1", n=(96, 80, 1), nt=15)
+        p = W.Problem(**dict(p.__dict__, time_order=2, space_order=8, dt=8e-4, dx=(10.0, 10.0, 10.0),
+                             init="zero", layers=(1500.0, 2500.0, 3500.0, 4500.0), f_peak=15.0,
+                             sponge=6, src=((48, 40, 0),)))
+    else:
+        p = W.problem("C1")
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    try:
+        r = SlabRunner(p, t_kernel=1, device=0)
+        host = r.host_inputs(p.nt, pin=False)
+        dev = r.to_device(host, p.nt)
+
+        def step():
+            r.reset_state(dev)
+            r.run(dev, p.nt)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            step()
+        op, oc, _ = oracle_run(p)
+        for _ in range(3):
+            dev["u_cur"].zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(r.stencil.interior(dev["u_cur"]).cpu().numpy(), oc)
+            assert np.array_equal(r.stencil.interior(dev["u_prev"]).cpu().numpy(), op)
+        r.stencil.close()
+    finally:
+        torch.cuda.set_stream(torch.cuda.default_stream())
