@@ -151,9 +151,11 @@ def run_gpu(args):
     else:
         tc = tk
     nt = p.nt if args.nt is None else args.nt
-    # launch-bound runs (the whole-run 2-D kernel: one launch of ~15 us per step) replay the step
-    # (state reset + stencil_run) as a CUDA graph captured on the plan's own stream
-    use_graph = (p.ndim == 2 and world == 1 and not args.no_graph)
+    # --graph (2-D, one rank): replay the step (stencil_run_from the stored initial fields) as a CUDA
+    # graph captured on the plan's own stream.  Off by default: the step is one resident launch,
+    # and direct calls let programmatic dependent launch overlap each launch with the previous
+    # kernel, which replays of a one-node graph do not (C1: 14.1 vs 16.4 us per step, DESIGN §6 G4)
+    use_graph = (p.ndim == 2 and world == 1 and args.graph)
     plan_stream = torch.cuda.Stream(device=local) if use_graph else torch.cuda.current_stream(local)
     if use_graph:
         torch.cuda.set_stream(plan_stream)     # every torch op, event and replay on the plan's stream
@@ -166,8 +168,9 @@ def run_gpu(args):
     fused = runner.enable_fused(dev_in) if args.fused_halo else False
 
     def step_resident():
-        runner.reset_state(dev_in)          # the initial fields (device copy, part of the step)
-        return runner.run(dev_in, nt)
+        # one simulation from the stored initial fields (a device copy of them is part of the
+        # step, except where the 2-D resident kernel loads them itself: stencil_run_from)
+        return runner.run_from_init(dev_in, nt)
 
     step_direct = step_resident
     graph = None
@@ -187,7 +190,7 @@ def run_gpu(args):
             print(f"bench.py: CUDA graph capture failed ({ex}); direct calls", file=sys.stderr)
             torch.cuda.synchronize()
     if graph is not None:
-        def step_resident():            # noqa: F811 -- the captured step (reset + stencil_run)
+        def step_resident():            # noqa: F811 -- the captured step (stencil_run_from)
             graph.replay()
 
     # clock sampler first (its start waits for the first nvidia-smi sample, an idle gap that would
@@ -278,7 +281,7 @@ def run_gpu(args):
                 "time_order": p.time_order, "t_kernel": tk, "t_comm": tc if world > 1 else None,
                 "schedule": pl.reason if args.tk == "auto" else f"t_kernel={tk} forced by --tk (planner: {pl.reason})",
                 "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
-                "step_launch": ("CUDA graph replay of one captured step (state reset + stencil_run)"
+                "step_launch": ("CUDA graph replay of one captured step (stencil_run_from the stored initial fields)"
                                 if graph is not None else "direct API calls"),
                 "halo": (None if world == 1 else
                          "fused push: sweep stores band planes into peer ghost zones (P2P)" if fused
@@ -483,7 +486,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=5, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="2-D runs: call the API per step instead of replaying a CUDA graph of it")
+    ap.add_argument("--graph", action="store_true", help="2-D runs: replay a CUDA graph of the step instead of calling the API per step")
     ap.add_argument("--fused-halo", action="store_true",
                     help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")
     ap.add_argument("--lib-exchange", action="store_true",

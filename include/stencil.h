@@ -152,6 +152,26 @@ st_status stencil_run_save(stencil_plan *p, float *u_prev, float *u_cur, const f
                            const int32_t *rec_xyz, float *rec_trace, int32_t save_every,
                            float *snapshots, int64_t snap_stride);
 
+/* stencil_run from an initial pair that is kept: (u_prev, u_cur) receive (u^{n+nt-1}, u^{n+nt}) of
+ * the run that starts from (init_prev, init_cur) = (u^{n-1}, u^n); the initial fields are not
+ * modified.  Same result as copying the two fields (X*Y*Z floats each) into u_prev / u_cur and
+ * calling stencil_run -- which is what it does on the plan's stream, except for the 2-D plans the
+ * whole-run resident kernel serves (SURVEY §8(a) a7 taken to the end: one launch per run), where
+ * that kernel loads the initial pair directly (one launch, no copy).  Use: repeated simulations
+ * (the paper's timed runs) from one stored initial condition.
+ *   init_prev, init_cur : device, layout above, read-only; heat: init_prev ignored (may be NULL).
+ *                         Each is either its own output buffer (init_cur == u_cur: no copy) or
+ *                         disjoint from both u_prev and u_cur.
+ *   the other arguments : as stencil_run.
+ * Errors: as stencil_run, plus ST_EINVAL for a NULL initial field or an initial field that
+ * overlaps an output field it is not identical to.  On an error reported after the copies were
+ * enqueued, u_prev / u_cur hold the initial pair. */
+st_status stencil_run_from(stencil_plan *p, const float *init_prev, const float *init_cur,
+                           float *u_prev, float *u_cur, const float *vel, const float *damp,
+                           int32_t nt, int64_t step0, int32_t nsrc, const int32_t *src_xyz,
+                           const float *src_wavelet, int32_t nrec, const int32_t *rec_xyz,
+                           float *rec_trace);
+
 /* 1 if the last stencil_run / stencil_run_save of p (created with ST_NO_SWAP) left the pair
  * swapped: u_prev then holds u^{n+nt} and u_cur holds u^{n+nt-1}, and the caller exchanges its two
  * references before the next run.  0 otherwise (always 0 without ST_NO_SWAP); -1 if p is NULL.

@@ -18,7 +18,8 @@ STATUS_NAMES = {0: "ST_OK", 1: "ST_EINVAL", 2: "ST_ENOMEM", 3: "ST_ECUDA", 4: "S
                 5: "ST_EUNSUPPORTED", 6: "ST_ESTATE"}
 
 # Every symbol include/stencil.h declares (checked by tests/test_abi_symbols.py).
-EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_run_save", "stencil_sync",
+EXPORTS = ("stencil_create", "stencil_layout", "stencil_run", "stencil_run_save", "stencil_run_from",
+           "stencil_sync",
            "stencil_destroy", "stencil_last_error", "stencil_supported", "stencil_abi_version",
            "stencil_set_timing", "stencil_timing", "stencil_swapped", "stencil_peer_counters",
            "stencil_set_peer", "stencil_ipc_export", "stencil_ipc_open", "stencil_nccl_unique_id")
@@ -75,6 +76,8 @@ def load():
     lib.stencil_run.restype = ctypes.c_int
     lib.stencil_run_save.argtypes = lib.stencil_run.argtypes + [ctypes.c_int32, P, ctypes.c_int64]
     lib.stencil_run_save.restype = ctypes.c_int
+    lib.stencil_run_from.argtypes = lib.stencil_run.argtypes[:1] + [P, P] + lib.stencil_run.argtypes[1:]
+    lib.stencil_run_from.restype = ctypes.c_int
     lib.stencil_sync.argtypes = [P]
     lib.stencil_sync.restype = ctypes.c_int
     lib.stencil_destroy.argtypes = [P]

@@ -770,7 +770,7 @@ static void plan_xtiles(const stencil_plan* p, const st::KernelEntry* k, int out
 
 // ------------------------------------------------------------------ resident 2-D run (G4)
 extern "C++" {
-typedef void (*res_kernel_t)(const st::SweepParams, float*, float*, int, int);
+typedef void (*res_kernel_t)(const st::SweepParams, float*, float*, const float*, const float*, int, int);
 template <int R>
 static res_kernel_t res_pick(bool wave) {
   return wave ? &st::resident2d_kernel<R, true> : &st::resident2d_kernel<R, false>;
@@ -806,7 +806,8 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
                           const int32_t* src_xyz, const float* src_wavelet, int32_t nrec,
                           const int32_t* rec_xyz, float* rec_trace, int32_t save_every,
                           float* snapshots, int64_t snap_stride, int zr_lo = -1, int zr_hi = -1,
-                          bool internal = false) {
+                          bool internal = false, const float* in_prev = nullptr,
+                          const float* in_cur = nullptr) {
   if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
   if (p->broken) return fail(p, ST_ESTATE, "plan is in an error state after an earlier CUDA fault");
   const st_config& c = p->cfg;
@@ -894,6 +895,8 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   int j = 0;
   int launches = 0, tiled_launches = 0;
   const bool resident = save_every <= 0 && !fused && zr_lo < 0 && res_fits(p);
+  // stencil_run_from hands the initial pair here only for runs the resident kernel serves
+  if (in_cur && !resident) return fail(p, ST_EINVAL, "internal: initial pair without a resident run");
   cudaEvent_t t_ev1 = nullptr;
   if (p->timing) {
     if ((int)p->ev_pool.size() < 2 * (p->ev_used + 1)) {
@@ -938,7 +941,8 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
       la[1].val.programmaticStreamSerializationAllowed = ST_PDL;
       lc.attrs = la;
       lc.numAttrs = 2;
-      le = cudaLaunchKernelEx(&lc, kf, sp, u_prev, u_cur, (int)nt, spb);
+      le = cudaLaunchKernelEx(&lc, kf, sp, u_prev, u_cur, (const float*)(in_cur ? in_prev : u_prev),
+                              (const float*)(in_cur ? in_cur : u_cur), (int)nt, spb);
       if (le == cudaSuccess) break;
       cudaGetLastError();
       if (cap == 8) break;
@@ -1303,6 +1307,40 @@ st_status stencil_run(stencil_plan* p, float* u_prev, float* u_cur, const float*
   }
   return run_impl(p, u_prev, u_cur, vel, damp, nt, step0, nsrc, src_xyz, src_wavelet, nrec, rec_xyz,
                   rec_trace, 0, nullptr, 0);
+}
+
+static bool overlaps(const void* a, const void* b, size_t bytes) {
+  const char* x = static_cast<const char*>(a);
+  const char* y = static_cast<const char*>(b);
+  return x < y + bytes && y < x + bytes;
+}
+
+st_status stencil_run_from(stencil_plan* p, const float* init_prev, const float* init_cur,
+                           float* u_prev, float* u_cur, const float* vel, const float* damp,
+                           int32_t nt, int64_t step0, int32_t nsrc, const int32_t* src_xyz,
+                           const float* src_wavelet, int32_t nrec, const int32_t* rec_xyz,
+                           float* rec_trace) {
+  if (!p) return fail(nullptr, ST_EINVAL, "plan is NULL");
+  const bool wave = p->cfg.time_order == 2;
+  if (!init_cur || (wave && !init_prev)) return fail(p, ST_EINVAL, "initial field pointer is NULL");
+  if (!u_prev || !u_cur) return fail(p, ST_EINVAL, "u_prev/u_cur is NULL");
+  const size_t fb = (size_t)p->X * p->Y * p->Z * sizeof(float);
+  // each initial field is either its own output buffer (no copy) or disjoint from both outputs
+  const float* ins[2] = {wave ? init_prev : nullptr, init_cur};
+  float* outs[2] = {u_prev, u_cur};
+  for (int i = 0; i < 2; ++i)
+    if (ins[i] && ins[i] != outs[i] && (overlaps(ins[i], u_prev, fb) || overlaps(ins[i], u_cur, fb)))
+      return fail(p, ST_EINVAL, "initial field %d overlaps an output field", i);
+  if (!p->comm && nt > 0 && !fused_ready(p) && res_fits(p))
+    // G4: the resident kernel loads the initial pair itself (no copy, one launch)
+    return run_impl(p, u_prev, u_cur, vel, damp, nt, step0, nsrc, src_xyz, src_wavelet, nrec, rec_xyz,
+                    rec_trace, 0, nullptr, 0, -1, -1, false, wave ? init_prev : u_prev, init_cur);
+  CK(cudaSetDevice(p->device), "cudaSetDevice");
+  for (int i = 0; i < 2; ++i)
+    if (ins[i] && ins[i] != outs[i])
+      CK(cudaMemcpyAsync(outs[i], ins[i], fb, cudaMemcpyDeviceToDevice, p->stream), "initial field copy");
+  return stencil_run(p, u_prev, u_cur, vel, damp, nt, step0, nsrc, src_xyz, src_wavelet, nrec, rec_xyz,
+                     rec_trace);
 }
 
 st_status stencil_run_save(stencil_plan* p, float* u_prev, float* u_cur, const float* vel,

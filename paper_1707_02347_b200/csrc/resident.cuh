@@ -126,14 +126,16 @@ __device__ __forceinline__ void res_strip(const float* C, float* out, const floa
 }
 
 // Cluster of cs CTAs (cluster dims (cs,1,1), grid (cs,1,1)); u_prev / u_cur in the library layout
+// (outputs; the initial pair is read from in_prev / in_cur, which may be u_prev / u_cur -- no
+// __restrict__: every CTA loads its rows before the first cluster barrier and stores after it)
 // (2-D: one plane, row pitch p.X).  Every spb steps the CTAs exchange an H = r*spb row halo (the
 // paper's ghost zone of depth r*T_c, here between the CTAs of a cluster) and
 // recompute it redundantly in between (rows shrinking by r per step), so one cluster barrier
 // serves spb steps.
 template <int R, bool WAVE>
 __global__ void __launch_bounds__(RES_THREADS, 1)
-resident2d_kernel(const __grid_constant__ SweepParams p, float* __restrict__ u_prev,
-                  float* __restrict__ u_cur, int nt, int spb) {
+resident2d_kernel(const __grid_constant__ SweepParams p, float* u_prev, float* u_cur,
+                  const float* in_prev, const float* in_cur, int nt, int spb) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) float sm[];
@@ -158,9 +160,10 @@ resident2d_kernel(const __grid_constant__ SweepParams p, float* __restrict__ u_p
   unsigned* sflag = reinterpret_cast<unsigned*>(sm + 2 * fsz + (WAVE ? 2 * nx2 * rows : 0));
   const int tid = threadIdx.x;
 
-  pdl_prologue_done();
+  // own shared memory first (nothing a predecessor grid writes), then wait for the predecessor
   for (int i = tid; i < 2 * fsz; i += RES_THREADS) sm[i] = 0.f;   // zero halo = Dirichlet
   for (int i = tid; i < (pr * rows + 31) / 32; i += RES_THREADS) sflag[i] = 0u;
+  pdl_prologue_done();
   __syncthreads();
   // u^n, u^{n-1} (wave) and a, c (wave): own rows + the halo rows inside the grid
   const int lo = max(0, r0 - H), hi = min(ny, r1 + H);
@@ -168,8 +171,8 @@ resident2d_kernel(const __grid_constant__ SweepParams p, float* __restrict__ u_p
     const int yy = i / nx, x = i - yy * nx;
     const int y = lo + yy;
     const int s = (y - r0 + H) * pitch + HL + x;
-    B1[s] = u_cur[(size_t)y * X + x];
-    if (WAVE) B0[s] = u_prev[(size_t)y * X + x];
+    B1[s] = in_cur[(size_t)y * X + x];
+    if (WAVE) B0[s] = in_prev[(size_t)y * X + x];
   }
   if (WAVE) {
     const int X2 = X >> 1;

@@ -208,6 +208,24 @@ class SlabRunner:
         if self.wave:           # heat reads only u^n: its u_prev is output-only (include/stencil.h)
             dev["u_prev"].copy_(dev["_init_prev"])
 
+    def run_from_init(self, dev, nt: int):
+        """One simulation from the stored initial pair (the bench step): on one rank
+        stencil_run_from (the 2-D resident kernel loads the pair itself: one launch, no copy; other
+        plans copy it on the plan's stream), else reset_state + run."""
+        if self.world > 1 or self.fused or self.lib_exchange:
+            self.reset_state(dev)
+            return self.run(dev, nt)
+        p, st = self.p, self.stencil
+        trace = dev.get("trace")
+        if trace is not None:
+            trace = trace[:nt]          # one rank owns every receiver: every entry is written
+        st.run(dev["u_prev"], dev["u_cur"], nt, vel=dev.get("vel"), damp=dev.get("damp"), step0=0,
+               src=list(p.src), wavelet=dev.get("wavelet"), rec=list(p.rec), trace=trace,
+               init=(dev["_init_prev"] if self.wave else None, dev["_init_cur"]))
+        if st.swapped():
+            dev["u_prev"], dev["u_cur"] = dev["u_cur"], dev["u_prev"]
+        return trace
+
     def upload(self, host, dev):
         for k in ("u_prev", "u_cur", "vel", "damp", "wavelet"):
             if k in host:

@@ -110,16 +110,21 @@ class Stencil:
             damp: Optional[torch.Tensor] = None, step0: int = 0, src=None,
             wavelet: Optional[torch.Tensor] = None, rec=None,
             trace: Optional[torch.Tensor] = None, save_every: int = 0,
-            snapshots: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+            snapshots: Optional[torch.Tensor] = None, init=None) -> Optional[torch.Tensor]:
         """Advance (u_prev, u_cur) by nt steps in place (asynchronous on the plan's stream).
         Returns the receiver trace tensor [nt, nrec] (allocated if not given).
         save_every > 0: also store u^{n + j*save_every}, j = 1..nt//save_every, into
-        snapshots[j-1] (a [nsnap, Z, Y, X] float32 CUDA tensor; stencil_run_save)."""
-        for t in (u_prev, u_cur, vel, damp, wavelet, trace):
+        snapshots[j-1] (a [nsnap, Z, Y, X] float32 CUDA tensor; stencil_run_save).
+        init = (init_prev, init_cur): start from this kept pair instead of (u_prev, u_cur), which
+        then only receive the result (stencil_run_from; heat: init_prev may be None)."""
+        init_prev, init_cur = (None, None) if init is None else init
+        if init is not None and (init_cur is None or save_every):
+            raise ValueError("init needs init_cur and does not combine with snapshots")
+        for t in (u_prev, u_cur, vel, damp, wavelet, trace, init_prev, init_cur):
             if t is not None:
                 if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
                     raise ValueError("fields/wavelet/trace must be contiguous float32 CUDA tensors")
-        for t in (u_prev, u_cur, vel, damp):
+        for t in (u_prev, u_cur, vel, damp, init_prev, init_cur):
             if t is not None and tuple(t.shape) != self.shape:
                 raise ValueError(f"field shape {tuple(t.shape)} != layout {self.shape}")
         nsrc, src_a = _points(src)
@@ -144,6 +149,8 @@ class Stencil:
                 raise ValueError("snapshots must be a contiguous float32 CUDA tensor [nt//save_every, Z, Y, X]")
             stride = self.shape[0] * self.shape[1] * self.shape[2]
             st = lib.stencil_run_save(*args, int(save_every), _ptr(snapshots), stride)
+        elif init is not None:
+            st = lib.stencil_run_from(args[0], _ptr(init_prev), _ptr(init_cur), *args[1:])
         else:
             st = lib.stencil_run(*args)
         _lib.check(st, self._h)
