@@ -236,19 +236,28 @@ def run_gpu(args):
     value = pts / (t_ms * 1e-3) / 1e9
 
     # ---- e2e: host pinned inputs in, results out, through the public API ---------------------
-    def step_e2e():
-        runner.upload(host, dev_in)
-        tr = runner.run(dev_in, nt)
-        return runner.download(dev_in, tr)
-    for _ in range(max(1, args.warmup // 2)):
-        step_e2e()
+    # default: pipelined over two device input slots (step k+1's upload and step k-1's read-back
+    # overlap step k's run, on their own streams; SlabRunner.run_host_pipelined); --e2e-serial:
+    # upload, run, read back one after the other on one stream
+    if args.e2e_serial:
+        def e2e_steps(k):
+            for _ in range(k):
+                runner.upload(host, dev_in)
+                tr = runner.run(dev_in, nt)
+                runner.download(dev_in, tr)
+    else:
+        dev_slots = [dev_in, runner.to_device(host, nt)]
+        io_streams = (torch.cuda.Stream(device=local), torch.cuda.Stream(device=local))
+
+        def e2e_steps(k):
+            runner.run_host_pipelined(host, dev_slots, nt, k, io_streams)
+    e2e_steps(max(1, args.warmup // 2))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for _ in range(args.steps):
-        step_e2e()
+    e2e_steps(args.steps)
     e3.record(stream)
     torch.cuda.synchronize()
     t_e2e = e2.elapsed_time(e3)
@@ -292,7 +301,10 @@ def run_gpu(args):
                     runner.field_bytes / 2**20),
             },
             "e2e": {"value": round(e2e_value, 3), "unit": "GPts/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "schedule": ("serial: upload, run, read back" if args.e2e_serial else
+                                 "pipelined: 2 device input slots; step k+1's H2D and step k-1's "
+                                 "D2H overlap step k's run (own streams)")},
             "gpu_launches": int(sweep_launches + aux),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -486,6 +498,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=5, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-serial", action="store_true",
+                    help="e2e: upload, run and read back each step serially (default: pipelined over two input slots)")
     ap.add_argument("--graph", action="store_true", help="2-D runs: replay a CUDA graph of the step instead of calling the API per step")
     ap.add_argument("--fused-halo", action="store_true",
                     help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")

@@ -231,17 +231,55 @@ class SlabRunner:
             if k in host:
                 dev[k].copy_(host[k], non_blocking=True)
 
-    def download(self, dev, trace):
+    def download(self, dev, trace, slot: int = 0):
+        """Asynchronous copy of u^{n+nt} (owned interior) and the trace into pinned host buffers
+        (one pair per slot, so pipelined steps never share a destination); returns them."""
         st = self.stencil
-        if not hasattr(self, "_out_host"):
-            self._out_host = torch.empty(st.interior(dev["u_cur"]).shape, dtype=torch.float32,
-                                         pin_memory=True)
-            self._tr_host = (torch.empty(trace.shape, dtype=torch.float32, pin_memory=True)
-                             if trace is not None else None)
-        self._out_host.copy_(st.interior(dev["u_cur"]), non_blocking=True)
+        if not hasattr(self, "_out_bufs"):
+            self._out_bufs = {}
+        if slot not in self._out_bufs:
+            self._out_bufs[slot] = (
+                torch.empty(st.interior(dev["u_cur"]).shape, dtype=torch.float32, pin_memory=True),
+                torch.empty(trace.shape, dtype=torch.float32, pin_memory=True) if trace is not None else None)
+        out_h, tr_h = self._out_bufs[slot]
+        out_h.copy_(st.interior(dev["u_cur"]), non_blocking=True)
         if trace is not None:
-            self._tr_host.copy_(trace, non_blocking=True)
-        return self._out_host, self._tr_host
+            tr_h.copy_(trace, non_blocking=True)
+        return out_h, tr_h
+
+    def run_host_pipelined(self, host, devs, nt: int, steps: int, streams):
+        """steps simulations, each from the pinned host inputs to pinned host results, pipelined
+        over the device input slots devs (to_device copies): step k uploads into slot k % len(devs)
+        on streams[0] while step k-1 runs on the plan's stream, and downloads on streams[1] while
+        step k+1 runs.  A slot is re-uploaded only after its previous results were read back.
+        Every step still copies all of its inputs in and its result out (bench.py e2e)."""
+        import torch
+        comp = self.stencil.stream
+        h2d, d2h = streams
+        free = [None] * len(devs)
+        res = None
+        h2d.wait_stream(comp)           # the first upload starts after the work already queued
+        for k in range(steps):
+            i = k % len(devs)
+            d = devs[i]
+            with torch.cuda.stream(h2d):
+                if free[i] is not None:
+                    h2d.wait_event(free[i])
+                self.upload(host, d)
+                up = torch.cuda.Event()
+                up.record(h2d)
+            with torch.cuda.stream(comp):
+                comp.wait_event(up)
+                tr = self.run(d, nt)
+                done = torch.cuda.Event()
+                done.record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                res = self.download(d, tr, slot=i)
+                free[i] = torch.cuda.Event()
+                free[i].record(d2h)
+        comp.wait_stream(d2h)
+        return res
 
     def io_bytes(self, host) -> Tuple[int, int]:
         h2d = sum(host[k].numel() * 4 for k in ("u_prev", "u_cur", "vel", "damp", "wavelet") if k in host)

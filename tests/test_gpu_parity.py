@@ -393,3 +393,34 @@ def test_run_from_kept_initial_pair(monkeypatch, case):
         st.run(P, C, 1, vel=vel, damp=damp, src=list(p.src), wavelet=wav, rec=list(p.rec),
                init=(I0 if wave else None, P))
     st.close()
+
+
+# ----------------------------------------------------------------------------- pipelined e2e (bench)
+@pytest.mark.parametrize("case", ["wave3d", "heat2d"])
+def test_host_pipelined_runs(case):
+    """SlabRunner.run_host_pipelined (bench.py's e2e): uploads, runs and read-backs of successive
+    simulations overlap on three streams over two device slots; every step's host result is the
+    oracle's bit for bit (checked on the last two steps, one per slot)."""
+    import torch
+    from paper_1707_02347_b200.dist import SlabRunner
+    if case == "wave3d":
+        p = _wave("C3", (45, 38, 30), 9, 5, src=[(22, 19, 15)], rec=[(20, 20, 20), (3, 4, 5)])
+    else:
+        p = W.problem("C1", n=(99, 128, 1), nt=23)
+    r = SlabRunner(p, t_kernel=1, device=0)
+    host = r.host_inputs(p.nt, pin=True)
+    devs = [r.to_device(host, p.nt), r.to_device(host, p.nt)]
+    streams = (torch.cuda.Stream(), torch.cuda.Stream())
+    op, oc, ot = oracle_run(p)
+    for steps in (1, 2, 5):
+        for d in devs:
+            d["u_cur"].fill_(float("nan"))
+        out = r.run_host_pipelined(host, devs, p.nt, steps, streams)
+        torch.cuda.synchronize()
+        assert np.array_equal(out[0].numpy().reshape(oc.shape), oc)
+        if p.rec:
+            assert np.array_equal(out[1].numpy(), ot)
+        if steps > 1:           # the other slot's result too
+            other = r._out_bufs[(steps - 2) % 2]
+            assert np.array_equal(other[0].numpy().reshape(oc.shape), oc)
+    r.stencil.close()
