@@ -239,7 +239,10 @@ def run_gpu(args):
     # default: pipelined over two device input slots (step k+1's upload and step k-1's read-back
     # overlap step k's run, on their own streams; SlabRunner.run_host_pipelined); --e2e-serial:
     # upload, run, read back one after the other on one stream
-    if args.e2e_serial:
+    # auto: serial for the launch-bound 2-D runs (C1: a 14 us run; the three-stream choreography's
+    # host cost per step exceeds it -- 3.8 vs 8.5 GPts/s measured), pipelined for 3-D
+    e2e_serial = args.e2e == "serial" or (args.e2e == "auto" and p.ndim == 2)
+    if e2e_serial:
         def e2e_steps(k):
             for _ in range(k):
                 runner.upload(host, dev_in)
@@ -302,7 +305,7 @@ def run_gpu(args):
             },
             "e2e": {"value": round(e2e_value, 3), "unit": "GPts/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "schedule": ("serial: upload, run, read back" if args.e2e_serial else
+                    "schedule": ("serial: upload, run, read back" if e2e_serial else
                                  "pipelined: 2 device input slots; step k+1's H2D and step k-1's "
                                  "D2H overlap step k's run (own streams)")},
             "gpu_launches": int(sweep_launches + aux),
@@ -498,8 +501,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=5, help="time steps per reference bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-serial", action="store_true",
-                    help="e2e: upload, run and read back each step serially (default: pipelined over two input slots)")
+    ap.add_argument("--e2e", choices=("auto", "pipelined", "serial"), default="auto",
+                    help="e2e schedule: pipelined over two device input slots, or upload/run/read back "
+                         "serially (auto: serial for 2-D, pipelined for 3-D)")
     ap.add_argument("--graph", action="store_true", help="2-D runs: replay a CUDA graph of the step instead of calling the API per step")
     ap.add_argument("--fused-halo", action="store_true",
                     help="N > 1, T_c = T_k = 1: halo exchange fused into the sweep over peer memory")
