@@ -226,8 +226,12 @@ class SlabRunner:
             dev["u_prev"], dev["u_cur"] = dev["u_cur"], dev["u_prev"]
         return trace
 
+    def _inputs(self):
+        # heat reads only u^n (its u_prev is output-only, include/stencil.h): u_prev is not an input
+        return ("u_prev", "u_cur", "vel", "damp", "wavelet") if self.wave else ("u_cur", "wavelet")
+
     def upload(self, host, dev):
-        for k in ("u_prev", "u_cur", "vel", "damp", "wavelet"):
+        for k in self._inputs():
             if k in host:
                 dev[k].copy_(host[k], non_blocking=True)
 
@@ -282,7 +286,7 @@ class SlabRunner:
         return res
 
     def io_bytes(self, host) -> Tuple[int, int]:
-        h2d = sum(host[k].numel() * 4 for k in ("u_prev", "u_cur", "vel", "damp", "wavelet") if k in host)
+        h2d = sum(host[k].numel() * 4 for k in self._inputs() if k in host)
         n_out = self.p.n[0] * self.p.n[1] * (self.nzl if self.p.ndim == 3 else 1)
         d2h = 4 * (n_out + (self.p.nt * len(self.p.rec) if self.p.rec else 0))
         return h2d, d2h
