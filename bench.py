@@ -254,7 +254,7 @@ def run_gpu(args):
 
         def e2e_steps(k):
             runner.run_host_pipelined(host, dev_slots, nt, k, io_streams)
-    e2e_steps(max(1, args.warmup // 2))
+    e2e_steps(max(1, args.warmup))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
