@@ -21,6 +21,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -115,7 +117,7 @@ struct stencil_plan {
   float* peer_ab[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][a/b] peer buffers
   unsigned long long* peer_ctr[2] = {nullptr, nullptr};              // neighbours' counters
   long long fused_runs = 0;            // fused runs issued since the peers were set
-  std::vector<void*> ipc_opened;       // handles opened by stencil_ipc_open (closed on destroy)
+  std::vector<std::string> ipc_opened; // handles opened by stencil_ipc_open (released on destroy)
   // library-owned halo exchange (st_config.nccl_id): communicator, comm stream, join events
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -392,6 +394,23 @@ st_status stencil_ipc_export(const stencil_plan* p, const void* dev_ptr, void* b
   return ST_OK;
 }
 
+// One mapping per exported allocation and process: a second cudaIpcOpenMemHandle of a handle that
+// is already open (two fields sub-allocated from one torch segment, or two plans with the same
+// neighbour) is refused by the runtime, so opens are shared and reference-counted.
+struct IpcMapping { void* base; int refs; };
+static std::mutex g_ipc_mu;
+static std::map<std::string, IpcMapping> g_ipc_open;
+
+static void ipc_release(const std::string& key) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  auto it = g_ipc_open.find(key);
+  if (it == g_ipc_open.end()) return;
+  if (--it->second.refs == 0) {
+    cudaIpcCloseMemHandle(it->second.base);
+    g_ipc_open.erase(it);
+  }
+}
+
 st_status stencil_ipc_open(stencil_plan* p, const void* blob, void** dev_ptr) {
   if (!p || !blob || !dev_ptr) return fail(p, ST_EINVAL, "null argument");
   CK(cudaSetDevice(p->device), "cudaSetDevice");
@@ -400,8 +419,19 @@ st_status stencil_ipc_open(stencil_plan* p, const void* blob, void** dev_ptr) {
   memcpy(&h, blob, sizeof h);
   memcpy(&off, static_cast<const char*>(blob) + 64, sizeof off);
   void* base = nullptr;
-  CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-  p->ipc_opened.push_back(base);
+  const std::string key(static_cast<const char*>(blob), sizeof h);
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_open.find(key);
+    if (it != g_ipc_open.end()) {
+      it->second.refs++;
+      base = it->second.base;
+    } else {
+      CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      g_ipc_open.emplace(key, IpcMapping{base, 1});
+    }
+  }
+  p->ipc_opened.push_back(key);
   *dev_ptr = static_cast<char*>(base) + off;
   return ST_OK;
 }
@@ -537,7 +567,7 @@ void stencil_destroy(stencil_plan* p) {
   if (p->staging.ptr) cudaFreeHost(p->staging.ptr);
   if (p->staging_ev) cudaEventDestroy(p->staging_ev);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
-  for (void* h : p->ipc_opened) cudaIpcCloseMemHandle(h);
+  for (const std::string& k : p->ipc_opened) ipc_release(k);
   free_buf(p->counters);
   free_buf(p->xtiles); free_buf(p->xwords); free_buf(p->xtrace);
   if (p->comm) { cudaStreamSynchronize(p->comm_stream); nccl().destroy(p->comm); }

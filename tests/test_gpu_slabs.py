@@ -155,6 +155,43 @@ def test_fused_halo_push_bitwise(world, order, sims):
         assert np.array_equal(g, w)
 
 
+@pytest.mark.parametrize("world,order", [(2, 8), (3, 12)])
+def test_fused_halo_push_ipc_processes(world, order, tmp_path):
+    """The fused push across PROCESSES (one per rank, all on cuda:0): peers' buffers and counters
+    are CUDA IPC mappings (stencil_ipc_export/open), the ranks take turns step by step (gloo
+    barriers; no kernel waits on an unfinished one).  Bit-exact vs the oracle."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ipc_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(rk), str(world), str(port), str(tmp_path),
+                               str(order), "48"], stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+             for rk in range(world)]
+    outs = []
+    try:
+        for pr in procs:
+            outs.append(pr.communicate(timeout=240)[0].decode(errors="replace"))
+    finally:
+        for pr in procs:
+            if pr.poll() is None:
+                pr.kill()
+    for rk, (pr, out) in enumerate(zip(procs, outs)):
+        assert pr.returncode == 0, f"rank {rk} failed:\n{out[-3000:]}"
+    p = _problem(order=order, nz=48)
+    res = [np.load(tmp_path / f"rank{rk}.npz") for rk in range(world)]
+    got = (np.concatenate([r["P"] for r in res]), np.concatenate([r["C"] for r in res]),
+           sum(r["T"] for r in res))
+    want = oracle.run_problem(p)
+    assert np.abs(want[1]).max() > 0
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
 def test_fused_halo_push_rejects_bad_plans():
     from paper_1707_02347_b200 import Stencil
     from paper_1707_02347_b200._lib import StencilError
