@@ -103,6 +103,7 @@ struct stencil_plan {
   float dtf = 0.f;
   // scratch
   Buf ac, p2, c2, tables;
+  Buf a_pl, c_pl, aflag;               // planar medium + a == -1 tile flags (KernelEntry::askip)
   // two-role exchange passes (sweepx.cuh): tile table and u32 words [ticket, fault, prog[ntiles]]
   Buf xtiles, xwords, xtrace;
   std::vector<st::XTile> xx;           // host copy of the uploaded tile table
@@ -203,9 +204,13 @@ __device__ __forceinline__ void medium_point(float v, float eta, float dtf, floa
   c = div_ftz(two_dt2, den);
 }
 
+// a_pl != nullptr (planar-medium kernels): a and c also as planar fp32 fields, and aflag (preset to
+// 1) cleared for every (plane, oy-row x 64-column tile) holding an interior point with a != -1.
 __global__ void medium_kernel(const float* __restrict__ vel, const float* __restrict__ damp,
                               float4* __restrict__ ac, int nx, int ny, long long X, long long plane,
-                              int z_lo, int nplanes, float dtf, float two_dt2) {
+                              int z_lo, int nplanes, float dtf, float two_dt2,
+                              float* __restrict__ a_pl, float* __restrict__ c_pl,
+                              unsigned char* __restrict__ aflag, int oy, int ntx, int nty) {
   const long long X2 = X >> 1;
   const long long per_plane = X2 * ny;
   const long long total = per_plane * nplanes;
@@ -225,6 +230,12 @@ __global__ void medium_kernel(const float* __restrict__ vel, const float* __rest
     medium_point(v.x, e.x, dtf, two_dt2, a0, c0);
     if (x + 1 < nx) medium_point(v.y, e.y, dtf, two_dt2, a1, c1);
     ac[z * (plane >> 1) + y * X2 + xp] = make_float4(a0, a1, c0, c1);   // plane/2 float4 per plane
+    if (a_pl) {
+      *reinterpret_cast<float2*>(a_pl + off) = make_float2(a0, a1);
+      *reinterpret_cast<float2*>(c_pl + off) = make_float2(c0, c1);
+      if (!(a0 == -1.0f) || (x + 1 < nx && !(a1 == -1.0f)))
+        aflag[(z * nty + y / oy) * ntx + (x >> 6)] = 0;
+    }
   }
 }
 
@@ -526,6 +537,14 @@ st_status stencil_create(const st_config* cfg, stencil_plan** out) {
   if (c.time_order == 2) {
     s = ensure_buf(p, p->ac, 2 * field_bytes, "medium a/c");
     if (s != ST_OK) return bail(s);
+    if (kt1->askip) {   // planar a, c and the a == -1 tile flags of the untiled static-ring kernel
+      if (kt1->ox != 64) return bail(fail(p, ST_EUNSUPPORTED, "planar-medium kernel with a tile width other than 64"));
+      s = ensure_buf(p, p->a_pl, field_bytes, "medium a (planar)");
+      if (s == ST_OK) s = ensure_buf(p, p->c_pl, field_bytes, "medium c (planar)");
+      if (s == ST_OK)
+        s = ensure_buf(p, p->aflag, (size_t)p->Z * ((p->ny + kt1->oy - 1) / kt1->oy) * ((p->nx + 63) / 64), "a == -1 tile flags");
+      if (s != ST_OK) return bail(s);
+    }
   }
   if (c.t_kernel > 1) {
     s = ensure_buf(p, p->p2, field_bytes, "ping-pong u_prev");
@@ -563,7 +582,7 @@ st_status stencil_layout(const stencil_plan* p, int64_t padded[3], int64_t origi
 void stencil_destroy(stencil_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  free_buf(p->ac); free_buf(p->p2); free_buf(p->c2); free_buf(p->tables);
+  free_buf(p->ac); free_buf(p->a_pl); free_buf(p->c_pl); free_buf(p->aflag); free_buf(p->p2); free_buf(p->c2); free_buf(p->tables);
   if (p->staging.ptr) cudaFreeHost(p->staging.ptr);
   if (p->staging_ev) cudaEventDestroy(p->staging_ev);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -883,9 +902,17 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   if (wave && vel) {
     const long long n = (p->X / 2) * p->Y * (zv_hi - zv_lo);
     const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)p->sm_count * 16);
+    const bool planar = p->k_t1->askip != 0;
+    const int fl_oy = p->k_t1->oy, fl_ntx = (int)((p->nx + 63) / 64), fl_nty = (int)((p->ny + fl_oy - 1) / fl_oy);
+    if (planar)
+      CK(cudaMemsetAsync(p->aflag.ptr, 1, (size_t)p->Z * fl_nty * fl_ntx, p->stream), "aflag reset");
     medium_kernel<<<blocks, 256, 0, p->stream>>>(vel, damp, static_cast<float4*>(p->ac.ptr), (int)p->nx, (int)p->ny,
                                                   p->X, plane, (int)zv_lo, (int)(zv_hi - zv_lo), p->dtf,
-                                                  (float)(2.0 * c.dt * c.dt));
+                                                  (float)(2.0 * c.dt * c.dt),
+                                                  planar ? static_cast<float*>(p->a_pl.ptr) : nullptr,
+                                                  planar ? static_cast<float*>(p->c_pl.ptr) : nullptr,
+                                                  planar ? static_cast<unsigned char*>(p->aflag.ptr) : nullptr,
+                                                  fl_oy, fl_ntx, fl_nty);
     CK(cudaGetLastError(), "medium kernel launch");
     p->have_medium = true;
     ++aux_launches;
@@ -899,11 +926,11 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   // buffers: 0 = caller P, 1 = caller C, 2 = scratch P2, 3 = scratch C2
   float* bufs[4] = {u_prev, u_cur, static_cast<float*>(p->p2.ptr), static_cast<float*>(p->c2.ptr)};
   int prev = 0, cur = 1;
-  CUtensorMap maps_t1[4], maps_tk[4], maps_p0[4], maps_u1[4], maps_l1[4], map_a0, map_a1;
+  CUtensorMap maps_t1[4], maps_tk[4], maps_p0[4], maps_u1[4], maps_l1[4], map_a0, map_a1, map_c_pl, map_a_pl;
   bool have_t1[4] = {false, false, false, false}, have_tk[4] = {false, false, false, false};
   bool have_l1[4] = {false, false, false, false};
   bool have_p0[4] = {false, false, false, false}, have_u1[4] = {false, false, false, false};
-  bool have_ac = false;
+  bool have_ac = false, have_pl = false;
   st::KernelMaps km{};
 
   st::SweepParams sp{};
@@ -913,6 +940,9 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
   sp.zv_lo = (int)zv_lo;
   sp.zv_hi = (int)zv_hi;
   sp.ac = static_cast<const float4*>(p->ac.ptr);
+  sp.aflag = static_cast<const unsigned char*>(p->aflag.ptr);
+  sp.fl_ntx = (int)((p->nx + 63) / 64);
+  sp.fl_nty = (int)((p->ny + p->k_t1->oy - 1) / p->k_t1->oy);
   sp.K0 = p->K0; sp.dt = p->dtf;
   memcpy(sp.W, p->W, sizeof sp.W);
   sp.iso = 1;
@@ -1018,6 +1048,16 @@ static st_status run_impl(stencil_plan* p, float* u_prev, float* u_cur, const fl
         have_u1[cur] = true;
       }
       km.p0 = maps_p0[prev]; km.a0 = map_a0; km.u1 = maps_u1[cur]; km.a1 = map_a1;
+      if (k->askip) {   // planar medium: a0 = c box, a1 = a box (same geometry as the u^{n-1} box)
+        if (!have_pl) {
+          s = encode_box(p, static_cast<const float*>(p->c_pl.ptr), p->nx, p->X, plane, k->ebw, k->eh0, &map_c_pl);
+          if (s == ST_OK)
+            s = encode_box(p, static_cast<const float*>(p->a_pl.ptr), p->nx, p->X, plane, k->ebw, k->eh0, &map_a_pl);
+          if (s != ST_OK) return s;
+          have_pl = true;
+        }
+        km.a0 = map_c_pl; km.a1 = map_a_pl;
+      }
     }
     // output plane range after j+steps of the nt steps covered by the ghost zones
     const long long shrink = (long long)(nt - j - steps) * c.radius;

@@ -37,6 +37,8 @@ struct KernelEntry {
   int ebw = 0, eh0 = 0, eh1 = 0;   // time-tiled kernel (wave): field box width, level-0 / level-1
                                    // box rows of the producer-streamed u^{n-1}, u^n, medium
   int fixed_slots = 0;             // > 0: the ring depth is compiled in (sweep1s_kernel)
+  int askip = 0;                   // 1: planar medium (maps.a0 = c box, maps.a1 = a box) and
+                                   //    SweepParams::aflag (a-box loads skipped where a == -1)
   int exch = 0;                    // 1: two-role exchange pass (sweepx.cuh): host builds a tile
                                    //    table; maps.u1 = u^{n+1} box map over the level-1 output
 };
@@ -198,7 +200,7 @@ constexpr KernelEntry make_entry1s() {
                 R, (size_t)S::SLOT_BYTES, (size_t)S::FIXED_BYTES,
                 &launch_sweep1s<R, WAVE, NCW, VY>, &query_sweep1s<R, WAVE, NCW, VY>, S::NS - R - 1};
   e.fixed_slots = S::NS;
-  if (S::TMAE) { e.ebw = 64; e.eh0 = S::OY; e.eh1 = S::OY; }   // host encodes the u^{n-1} / medium maps
+  if (S::TMAE) { e.ebw = 64; e.eh0 = S::OY; e.eh1 = S::OY; e.askip = 1; }   // host encodes the u^{n-1} / medium maps
   return e;
 }
 

@@ -39,6 +39,11 @@ struct SweepParams {
   float* outC;                // TK>1: u^{n+TK}
   float* outS;                // snapshot of this pass's last level (same layout), or nullptr
   const float4* ac;           // medium {a(x),a(x+1),c(x),c(x+1)} per column pair; row = X/2 float4
+  // planar-medium kernels (KernelEntry::askip): one byte per (array plane, tile row, tile column),
+  // 1 where a == -1 at every interior point of the tile's plane (no damping there: the a box is
+  // not loaded), index (z * fl_nty + tile_y) * fl_ntx + tile_x
+  const unsigned char* aflag;
+  int fl_ntx, fl_nty;
   int write_prev;             // TK>1 heat: also write u^{n+TK-1}
   unsigned zero;              // always 0 (see zero_after)
   float K0, dt;

@@ -21,6 +21,12 @@
 
 namespace st {
 
+__device__ __forceinline__ uint32_t ld_flag(const unsigned char* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 #ifndef ST_S1S_TMAE
 #define ST_S1S_TMAE 1   // 1: u^{n-1} and the medium arrive by TMA (second producer warp, E ring);
                         // 0: per-warp cp.async staging (round-1 design, for A/B builds)
@@ -36,11 +42,13 @@ struct Geom1S {
   static constexpr int SMEM_MAX = 227 * 1024;
   static constexpr int BAR_BYTES = 1024;
   static constexpr bool TMAE = WAVE && ST_S1S_TMAE;
-  // TMA E ring (TMAE): per output plane, the tile's u^{n-1} box (64 x OY) then its medium box
-  // ({a,a,c,c} per pair: 128 floats x OY); DE entries, as many as shared memory allows (<= 8)
+  // TMA E ring (TMAE): per output plane, the tile's u^{n-1} box (64 x OY), its c box and its a
+  // box (planar medium, 64 x OY each); the a box is loaded only where the tile's plane holds a
+  // point with a != -1 (damping; SweepParams::aflag) -- elsewhere a is the constant -1 and the
+  // sweep moves 16 instead of 20 B/update; DE entries, as many as shared memory allows (<= 8)
   static constexpr int OY = NCW * VY;
   static constexpr int E_FIELD = (64 * OY * 4 + 127) / 128 * 128;
-  static constexpr int E_BYTES = E_FIELD + 128 * OY * 4;
+  static constexpr int E_BYTES = 3 * E_FIELD;
   static constexpr int DE_FIT = (SMEM_MAX - BAR_BYTES - NS * SLOT_BYTES) / E_BYTES;
   static constexpr int DE = DE_FIT > 8 ? 8 : DE_FIT;
   static constexpr int stage_bytes(int pd) { return NCW * (pd + 1) * STAGE_F * 4; }
@@ -76,6 +84,7 @@ sweep1s_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ 
   uint64_t* empty = full + NS;
   uint64_t* efull = full + 2 * NS;                // E ring (TMAE)
   uint64_t* eempty = efull + 8;
+  volatile uint32_t* eflag = reinterpret_cast<volatile uint32_t*>(eempty + 8);   // per E entry: a == -1
   float* stage0 = reinterpret_cast<float*>(smem + S::BAR_BYTES);
   float* ring = reinterpret_cast<float*>(smem + S::FIXED_BYTES);
 
@@ -109,11 +118,20 @@ sweep1s_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ 
       int es = 0;
       uint32_t eph = 0;
       const uint32_t ebase = smem_u32(smem + S::BAR_BYTES);
+      const long long fl_stride = (long long)p.fl_nty * p.fl_ntx;
+      const unsigned char* fl = p.aflag + zb * fl_stride + (long long)blockIdx.y * p.fl_ntx + blockIdx.x;
+      uint32_t f_next = ld_flag(fl);
       for (int s = zb; s < ze; ++s) {
+        const uint32_t f = f_next;                       // 1: a == -1 on this tile's plane s
+        fl += fl_stride;
+        if (s + 1 < ze) f_next = ld_flag(fl);            // in flight across the wait below
         if (s - zb >= DE) mbar_wait(&eempty[es], eph ^ 1u);
-        mbar_expect_tx(&efull[es], (uint32_t)(192 * S::OY * 4));   // both boxes, OOB zero-filled
+        eflag[es] = f;                                   // released to the consumers by the arrive
+        mbar_expect_tx(&efull[es], (uint32_t)((f ? 2 : 3) * 64 * S::OY * 4));   // OOB zero-filled
         tma_load_3d_s(ebase + es * EB, &maps.p0, smem_u32(&efull[es]), tx0, ty0, s - p.zv_lo);
-        tma_load_3d_s(ebase + es * EB + S::E_FIELD, &maps.a0, smem_u32(&efull[es]), 2 * tx0, ty0, s - p.zv_lo);
+        tma_load_3d_s(ebase + es * EB + S::E_FIELD, &maps.a0, smem_u32(&efull[es]), tx0, ty0, s - p.zv_lo);
+        if (!f)
+          tma_load_3d_s(ebase + es * EB + 2 * S::E_FIELD, &maps.a1, smem_u32(&efull[es]), tx0, ty0, s - p.zv_lo);
         if (++es == DE) { es = 0; eph ^= 1u; }
       }
     }
@@ -202,7 +220,8 @@ sweep1s_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ 
   // E ring (TMAE): my u^{n-1} pair and medium float4 of row j inside an entry
   const float* e_slot = reinterpret_cast<const float*>(smem + S::BAR_BYTES);
   const int e_pv = (warp * VY) * 64 + 2 * lane;
-  const int e_ac = S::E_FIELD / 4 + (warp * VY) * 128 + 4 * lane;
+  const int e_c = S::E_FIELD / 4 + e_pv, e_a = 2 * (S::E_FIELD / 4) + e_pv;
+  const uint64_t NEG1 = splat(-1.0f);
   int es = 0;
   uint32_t eph = 0;
 
@@ -224,16 +243,20 @@ sweep1s_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ 
     }
     uint64_t o[VY];
     if (TMAE) {
+      // (loading the E entry before the Laplacian measured no faster: C5 304.0 vs 306.6 GPts/s)
       mbar_wait(&efull[es], eph);
       const float* e = e_slot + es * (EB / 4);
-      uint32_t z = 0;
+      const uint32_t aneg = eflag[es];            // a == -1 on this plane of the tile: no a box
+      uint32_t z = aneg & p.zero;
 #pragma unroll
       for (int j = 0; j < VY; ++j) {
         const uint64_t c = qn[CS][j];
         const uint64_t pv = lds64(e + e_pv + j * 64);
-        const float4 m4 = *reinterpret_cast<const float4*>(e + e_ac + j * 128);
-        z |= zero_after(pv, p.zero) | zero_after(pack2(m4.x, m4.w), p.zero);
-        o[j] = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c)) & mask[j];
+        const uint64_t cv = lds64(e + e_c + j * 64);
+        uint64_t av = NEG1;
+        if (!aneg) av = lds64(e + e_a + j * 64);
+        z |= zero_after(pv | cv | av, p.zero);
+        o[j] = f2fma(cv, acc[j], f2fma(av, f2sub(pv, c), c)) & mask[j];
       }
       mbar_arrive(&eempty[es] + z);      // release the entry once my loads from it have returned
       if (++es == DE) { es = 0; eph ^= 1u; }

@@ -1,0 +1,8 @@
+#!/bin/bash
+# Planar medium with the a-box skipped where a == -1 (sweep1s): parity subset, then C5/C4 lines.
+set -u
+O=gpurun_out/askip; mkdir -p $O
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_slabs.py -m gpu -q -x > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
+timeout 600 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_C5.json 2> $O/bench_C5.err
+timeout 600 python bench.py --config C4 --steps 2 --warmup 3 --no-cpu-baseline > $O/bench_C4.json 2> $O/bench_C4.err
+echo done > $O/done.txt
