@@ -311,6 +311,11 @@ def run_gpu(args):
             "gpu_launches": int(sweep_launches + aux),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
+                         # DRAM bytes of the committed ncu capture over THIS run's launch time:
+                         # below `frac` where the kernel moves fewer bytes than the algorithmic
+                         # figure (the untiled wave kernel skips the a box where a == -1)
+                         "traffic_frac": (None if traffic is None or world > 1 else
+                                          round(traffic / (per_launch_ms * 1e-3) / 1e9 / peak, 4)),
                          "kernel": _kernel_name(p, tk), "alg_bytes_per_point_launch": bpp,
                          "per_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src},
             "clocks": ck,

@@ -33,8 +33,10 @@
  *   interior point (x, y, z_local) lives at [G + z_local][y][x].
  *
  * Ownership: the caller owns every field, wavelet and trace.  The library owns the plan and
- * its device scratch (medium a/c in an interleaved layout, the ping-pong pair for
- * t_kernel > 1, source/receiver tables).  It never frees caller memory.
+ * its device scratch (medium a/c in an interleaved layout -- 8 B per point -- plus, for the 3-D
+ * wave at radius 5, 6 and 8, a planar copy of a and c -- another 8 B per point -- and one flag byte
+ * per tile and plane; the ping-pong pair for t_kernel > 1; source/receiver tables).  It never
+ * frees caller memory.
  *
  * Errors: every entry returns st_status; nothing aborts, exits or throws across the ABI.
  * The message of the last failure is available from stencil_last_error().

@@ -74,6 +74,20 @@ def test_wave_orders_ragged(order, tk):
     _check(_wave("C3", n, 17, 8, order=order, src=src, rec=rec), t_kernel=tk)
 
 
+@pytest.mark.parametrize("order", [10, 12, 16])
+@pytest.mark.parametrize("sponge", [6, 0])
+def test_wave_undamped_tiles(order, sponge):
+    """The static-ring untiled kernel loads the a box only where a tile's plane holds a point
+    with a != -1 (a == -1 exactly where damp = 0; the medium kernel's tile flags).  A grid wide
+    enough for tiles (64 columns x 24 or 16 rows) that lie wholly inside the sponge-free interior,
+    next to tiles and planes that do not, and the same grid with no damping at all (every flag
+    set, boundary tiles included); sources in a skipped tile, in a damped tile and on the edge."""
+    n = (200, 110, 40)
+    src = [(100, 60, 20), (3, 4, 2), (199, 109, 39), (64, 48, 6)]
+    rec = [(100, 60, 20), (65, 49, 7), (127, 71, 33), (128, 72, 34), (2, 100, 20), (190, 30, 5)]
+    _check(_wave("C5", n, 11, sponge, order=order, src=src, rec=rec), t_kernel=1)
+
+
 @pytest.mark.parametrize("order", [12, 14, 16])
 @pytest.mark.parametrize("dx", [(10.0, 10.0, 10.0), (10.0, 12.5, 8.0)])
 def test_wave_isotropic_and_anisotropic_weights(order, dx):

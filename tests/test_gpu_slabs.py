@@ -229,6 +229,20 @@ def test_emulated_slabs_orders(order):
         assert np.array_equal(g, w)
 
 
+@pytest.mark.parametrize("order,tc", [(12, 1), (16, 2)])
+def test_emulated_slabs_undamped_tiles(order, tc):
+    """z-slab plans on a grid with tiles wholly inside the sponge-free interior: the a == -1 tile
+    flags (a box not loaded) are per slab plane, ghost planes included."""
+    p = W.problem("C5", n=(200, 80, 48), nt=9, sponge=5)
+    p = W.Problem(**{**p.__dict__, "space_order": order, "src": ((100, 40, 24), (70, 30, 23)),
+                     "rec": ((100, 40, 24), (65, 25, 23), (1, 1, 0), (199, 79, 47))})
+    got = _run_slabs(p, 2, 1, tc)
+    want = oracle.run_problem(p)
+    assert np.abs(want[1]).max() > 0
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
 @pytest.mark.parametrize("world,tk,tc", [(2, 4, 4), (3, 3, 6), (2, 2, 4), (4, 4, 8)])
 def test_emulated_slabs_heat_tiled(world, tk, tc):
     """Heat z-slabs on the register-resident time-tiled kernel (sweeph): ghost zones of depth
