@@ -150,7 +150,7 @@ constexpr KernelEntry make_entry1() {
   KernelEntry e{NDIM, WAVE ? 2 : 1, R, 1, VY, NCW, GE::NTHREADS, G::OX, G::OY, G::BW, G::BH,
                 G::RZ, (size_t)G::SLOT_BYTES, (size_t)GE::FIXED_BYTES,
                 &launch_sweep1<R, WAVE, NDIM, NCW, VY>, &query_sweep1<R, WAVE, NDIM, NCW, VY>, ST_T1_DEPTH};
-  if (GE::TMAE) { e.ebw = 64; e.eh0 = GE::OY; e.eh1 = GE::OY; }   // host encodes the u^{n-1} / medium maps
+  if (GE::TMAE) { e.ebw = 64; e.eh0 = GE::OY; e.eh1 = GE::OY; e.askip = 1; }   // host encodes the u^{n-1} / medium maps
   return e;
 }
 

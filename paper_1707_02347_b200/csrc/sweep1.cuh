@@ -93,8 +93,16 @@ struct Geom1 {
 #ifndef ST_S1_TMAE
 #define ST_S1_TMAE 1    // 3-D wave: u^{n-1} and the medium arrive by TMA (E ring, second producer warp)
 #endif
-// E ring of the untiled 3-D wave kernels: per output plane, the tile's u^{n-1} box (64 x OY) and
-// its medium box ({a,a,c,c} per pair: 128 floats x OY), DE entries.  TMA writes into shared memory
+// one flag byte of SweepParams::aflag (read-only for the whole launch)
+__device__ __forceinline__ uint32_t ld_flag(const unsigned char* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// E ring of the untiled 3-D wave kernels: per output plane, the tile's u^{n-1} box (64 x OY), its
+// c box and -- only where the tile's plane holds a point with a != -1 (SweepParams::aflag) -- its
+// a box (planar medium, 64 x OY each), DE entries.  TMA writes into shared memory
 // do not use the 128 B/clk/SM LDS crossbar that cp.async staging fills twice.
 template <int R, int NDIM, int NCW, int VY, bool WAVE>
 struct Geom1E {
@@ -102,7 +110,7 @@ struct Geom1E {
   static constexpr bool TMAE = WAVE && NDIM == 3 && R >= 3 && ST_S1_TMAE;
   static constexpr int OY = NCW * VY;
   static constexpr int E_FIELD = (64 * OY * 4 + 127) / 128 * 128;
-  static constexpr int E_BYTES = E_FIELD + 128 * OY * 4;
+  static constexpr int E_BYTES = 3 * E_FIELD;
   static constexpr int DE = 4;
   static constexpr int NPROD = TMAE ? 2 : 1;
   static constexpr int NTHREADS = 32 * (NCW + NPROD);
@@ -146,6 +154,7 @@ sweep1_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
   uint64_t* empty = full + nslot;
   uint64_t* efull = full + 112;                  // E ring barriers (TMAE), bytes 896..1023
   uint64_t* eempty = efull + 8;
+  volatile uint32_t* eflag = reinterpret_cast<volatile uint32_t*>(efull + 4);   // per E entry: a == -1 (DE = 4)
   float* ring = reinterpret_cast<float*>(smem + GE::FIXED_BYTES);
 
   const int tid = threadIdx.x;
@@ -178,12 +187,20 @@ sweep1_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
       int es = 0;
       uint32_t eph = 0;
       const uint32_t ebase = static_cast<uint32_t>(__cvta_generic_to_shared(smem + GE::BAR_BYTES));
+      const long long fl_stride = (long long)p.fl_nty * p.fl_ntx;
+      const unsigned char* fl = p.aflag + zb * fl_stride + (long long)blockIdx.y * p.fl_ntx + blockIdx.x;
+      uint32_t f_next = ld_flag(fl);
       for (int s = zb; s < ze; ++s) {
+        const uint32_t f = f_next;                       // 1: a == -1 on this tile's plane s
+        fl += fl_stride;
+        if (s + 1 < ze) f_next = ld_flag(fl);            // in flight across the wait below
         if (s - zb >= DE) mbar_wait(&eempty[es], eph ^ 1u);
-        mbar_expect_tx(&efull[es], (uint32_t)(192 * GE::OY * 4));   // both boxes, OOB zero-filled
+        eflag[es] = f;                                   // released to the consumers by the arrive
+        mbar_expect_tx(&efull[es], (uint32_t)((f ? 2 : 3) * 64 * GE::OY * 4));   // OOB zero-filled
         const uint32_t fb = static_cast<uint32_t>(__cvta_generic_to_shared(&efull[es]));
         tma_load_3d_e(ebase + es * EB, &maps.p0, fb, tx0, ty0, s - p.zv_lo);
-        tma_load_3d_e(ebase + es * EB + GE::E_FIELD, &maps.a0, fb, 2 * tx0, ty0, s - p.zv_lo);
+        tma_load_3d_e(ebase + es * EB + GE::E_FIELD, &maps.a0, fb, tx0, ty0, s - p.zv_lo);
+        if (!f) tma_load_3d_e(ebase + es * EB + 2 * GE::E_FIELD, &maps.a1, fb, tx0, ty0, s - p.zv_lo);
         if (++es == DE) { es = 0; eph ^= 1u; }
       }
     }
@@ -276,7 +293,8 @@ sweep1_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
   }
   const float* e_slot = reinterpret_cast<const float*>(smem + GE::BAR_BYTES);
   const int e_pv = (warp * VY) * 64 + 2 * lane;
-  const int e_ac = GE::E_FIELD / 4 + (warp * VY) * 128 + 4 * lane;
+  const int e_c = GE::E_FIELD / 4 + e_pv, e_a = 2 * (GE::E_FIELD / 4) + e_pv;
+  const uint64_t NEG1 = splat(-1.0f);
   int es = 0;
   uint32_t eph = 0;
 
@@ -325,14 +343,17 @@ sweep1_kernel(const __grid_constant__ KernelMaps maps, const __grid_constant__ S
           if (TMAE) {
             mbar_wait(&efull[es], eph);
             const float* e = e_slot + es * (EB / 4);
-            uint32_t z = 0;
+            const uint32_t aneg = eflag[es];        // a == -1 on this plane of the tile: no a box
+            uint32_t z = aneg & p.zero;
 #pragma unroll
             for (int j = 0; j < VY; ++j) {
               const uint64_t c = qn[md<QN>(u - RZ)][j];
               const uint64_t pv = lds64(e + e_pv + j * 64);
-              const float4 m4 = *reinterpret_cast<const float4*>(e + e_ac + j * 128);
-              z |= zero_after(pv, p.zero) | zero_after(pack2(m4.x, m4.w), p.zero);
-              o[j] = f2fma(pack2(m4.z, m4.w), acc[j], f2fma(pack2(m4.x, m4.y), f2sub(pv, c), c)) & mask[j];
+              const uint64_t cv = lds64(e + e_c + j * 64);
+              uint64_t av = NEG1;
+              if (!aneg) av = lds64(e + e_a + j * 64);
+              z |= zero_after(pv | cv | av, p.zero);
+              o[j] = f2fma(cv, acc[j], f2fma(av, f2sub(pv, c), c)) & mask[j];
             }
             mbar_arrive(&eempty[es] + z);    // release the entry once my loads from it have returned
             if (++es == DE) { es = 0; eph ^= 1u; }

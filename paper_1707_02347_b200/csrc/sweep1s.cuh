@@ -21,12 +21,6 @@
 
 namespace st {
 
-__device__ __forceinline__ uint32_t ld_flag(const unsigned char* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-
 #ifndef ST_S1S_TMAE
 #define ST_S1S_TMAE 1   // 1: u^{n-1} and the medium arrive by TMA (second producer warp, E ring);
                         // 0: per-warp cp.async staging (round-1 design, for A/B builds)
