@@ -34,7 +34,7 @@
  *
  * Ownership: the caller owns every field, wavelet and trace.  The library owns the plan and
  * its device scratch (medium a/c in an interleaved layout -- 8 B per point -- plus, for the 3-D
- * wave at radius 5, 6 and 8, a planar copy of a and c -- another 8 B per point -- and one flag byte
+ * wave at radius >= 3, a planar copy of a and c -- another 8 B per point -- and one flag byte
  * per tile and plane; the ping-pong pair for t_kernel > 1; source/receiver tables).  It never
  * frees caller memory.
  *
